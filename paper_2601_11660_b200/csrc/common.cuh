@@ -1,0 +1,123 @@
+// Shared helpers for libmbunet (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "../../include/mbunet.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libmbunet is written for sm_100a (B200) only"
+#endif
+
+namespace mbu {
+
+// thread-local last-error message behind mbu_last_error()
+void set_error(const std::string &msg);
+int fail(int status, const std::string &msg);
+extern std::atomic<int64_t> g_launches;
+extern int g_last_path;
+
+inline int check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return fail(MBU_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return MBU_OK;
+}
+
+inline int check_cuda(cudaError_t e, const char *what) {
+  if (e != cudaSuccess)
+    return fail(MBU_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return MBU_OK;
+}
+
+#define MBU_TRY(expr)              \
+  do {                             \
+    int _st = (expr);              \
+    if (_st != MBU_OK) return _st; \
+  } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------------------
+// threshold codes (layers.py:66-70): 0 GE, 1 LE, 2 const -1, 3 const +1
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool fires(int acc, int t, int code) {
+  return (code == 0) ? (acc >= t) : (code == 1) ? (acc <= t) : (code == 3);
+}
+
+struct ActView {        // packed activation view, see include/mbunet.h
+  const uint64_t *base;
+  int n, h, w;
+  int wpp;              // words per pixel of this tensor
+  int stride;           // words between consecutive pixels
+  int offset;           // word offset of this tensor inside each pixel slot
+};
+
+}  // namespace mbu
+
+// ---------------------------------------------------------------------------
+// the conv handle (definition shared by the generic and tcgen05 paths)
+// ---------------------------------------------------------------------------
+struct mbu_conv {
+  int device = 0;
+  int transposed = 0;
+  int kh = 0, kw = 0, stride = 1, pad = 0, c_in = 0, c_out = 0;
+  int pad_mode = 0;
+  int masked = 0;
+  int lpp = 0, wpp = 0;          // input lanes / words per pixel
+  int k_true = 0;                // kh*kw*c_in (binary XOR form)
+  int out_wpp = 0;               // ceil(c_out/128)*2
+  int has_threshold = 0;
+  uint64_t *d_pos = nullptr;     // [c_out][taps*wpp] reference layout
+  uint64_t *d_neg = nullptr;
+  int32_t *d_wsum = nullptr;     // [c_out][taps] signed sums (zero padding)
+  int32_t *d_thr = nullptr;      // [n_pad] thresholds
+  uint8_t *d_codes = nullptr;    // [n_pad] codes (pad channels = const -1)
+  // tcgen05 implicit-GEMM operand (see conv_tc.cu)
+  int tc_ok = 0;
+  int taps = 0;                  // 9 (3x3 conv) or 1 (1x1 conv / tconv)
+  int n_gemm = 0;                // GEMM N (c_out, or s*s*c_out_pad for tconv)
+  int n_pad = 0;                 // padded GEMM N (multiple of 32)
+  int c_out_pad = 0;             // tconv: per-tap padded c_out
+  int n_tile = 0;                // N per CTA tile
+  int n_tiles = 0;
+  int kc = 0;                    // active 32-lane chunks per pixel
+  int chunks_per_stage = 0;      // 32-lane chunks per pipeline stage
+  int n_stages_k = 0;            // K stages per tile (= ceil(kc / chunks_per_stage))
+  int32_t *d_chunk_word = nullptr;  // [kc] u32 index inside a pixel for each chunk
+  int8_t *d_b = nullptr;         // repacked s8 weights, UMMA K-major core-matrix order
+  size_t b_stage_bytes = 0;      // bytes of B per (n tile, K stage)
+};
+
+struct mbu_fconv {
+  int device = 0;
+  int kh = 0, kw = 0, stride = 1, pad = 0, c_in = 0, c_out = 0;
+  int has_bn = 0, has_bias = 0, bits_input = 0;
+  double *d_w = nullptr;      // (c_out, kh, kw, c_in)
+  double *d_bias = nullptr;
+  double *d_bn = nullptr;     // gamma, beta, mean, sigma (4*c_out)
+  int32_t *d_lanes = nullptr; // input lane per channel (bits input)
+};
+
+namespace mbu {
+// launchers implemented in generic.cu / conv_tc.cu
+int launch_conv_popcount(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
+                         uint64_t *bits, int out_stride, int out_offset, cudaStream_t st);
+int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
+                   uint64_t *bits, int out_stride, int out_offset, cudaStream_t st);
+int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg,
+                    const int32_t *seg_off, const int32_t *seg_cnt, int n_seg);
+int launch_maxpool(const ActView &x, uint64_t *out, int out_stride, int out_offset,
+                   cudaStream_t st);
+int launch_fconv(const mbu_fconv *fc, const double *x_f64, const ActView &xb, int n, int h,
+                 int w, double *acc, uint64_t *bits, int out_stride, int out_offset,
+                 uint8_t *mask, cudaStream_t st);
+int conv_run(mbu_conv *cv, const ActView &x, int32_t *acc, uint64_t *bits, int out_stride,
+             int out_offset, int path, cudaStream_t st);
+}  // namespace mbu

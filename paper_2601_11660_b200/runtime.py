@@ -1,0 +1,262 @@
+"""The MBU-Net forward on the GPU: model upload, planning, CUDA-graph replay.
+
+``forward(model, image, threads=1, trace=False)`` is the drop-in for
+``bitunet.graph.forward`` (``pkg/src/bitunet/graph.py:413-458``): same
+arguments, same :class:`ForwardResult` (float64 logits, uint8 mask, and with
+``trace=True`` a ``{name: {"acc", "out"}}`` dict whose bit outputs are
+:class:`BitTensor` objects byte-identical to the reference's).
+
+Underneath, :class:`DeviceModel` uploads each compiled layer once
+(``mbu_conv_create`` repacks the w+/w- planes for the tensor cores) and hands
+them to the native runner (``mbu_model_*``), which plans every activation as
+a view into one workspace and enqueues the whole network on a stream.
+:class:`Engine` adds persistent device buffers and a captured CUDA graph for
+steady-state throughput (bench.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import weakref
+
+import numpy as np
+import torch
+
+from . import _lib
+from .bitcore import BitTensor, ChannelSegment, segment_lane_table, segment_lanes
+from .errors import EngineError, ShapeError, UnsupportedConfigError
+from .ops import ConvHandle, FloatConvHandle, _ptr, _stream, cuda_device
+
+__all__ = ["DeviceModel", "Engine", "forward", "ForwardResult"]
+
+
+def _result_cls():
+    from .graph import ForwardResult
+
+    return ForwardResult
+
+
+ForwardResult = None  # resolved lazily (graph imports runtime lazily too)
+
+
+class DeviceModel:
+    """A compiled model resident on one GPU, driven by the native runner."""
+
+    def __init__(self, model, device=None):
+        self.device = cuda_device(device)
+        self.config = model.config
+        self.names, self.kinds = [], []
+        self.out_segments = []  # per layer: output lane layout (bit layers)
+        self.out_channels = []  # per layer: logical channel count
+        h = ctypes.c_void_p()
+        _lib.call("mbu_model_create", ctypes.byref(h), self.device.index)
+        self.handle = h
+        index = {}
+        segs = ()
+        cur_c = model.config.in_channels
+        seen_float = False
+        with torch.cuda.device(self.device):
+            for i, layer in enumerate(model.layers):
+                kind = layer.kind
+                if kind == "float-conv":
+                    lanes = None
+                    if seen_float or i > 0:
+                        lanes = segment_lane_table(segs)
+                    fc = FloatConvHandle(layer.weights, layer.bias, layer.spec,
+                                         bn=layer.bn if layer.apply_sign else None,
+                                         in_lanes=lanes, device=self.device)
+                    _lib.call("mbu_model_add_fconv", h, fc.release(), int(bool(layer.apply_sign)))
+                    seen_float = True
+                    segs = (ChannelSegment(0, layer.spec.c_out),)
+                    cur_c = layer.spec.c_out
+                elif kind in ("binary-conv", "masked-conv", "binary-tconv", "masked-tconv"):
+                    cv = ConvHandle(layer.weights, layer.spec, segs, layer.threshold,
+                                    transposed=kind.endswith("tconv"), device=self.device)
+                    _lib.call("mbu_model_add_conv", h, cv.release())
+                    segs = (ChannelSegment(0, layer.spec.c_out),)
+                    cur_c = layer.spec.c_out
+                elif kind == "maxpool":
+                    _lib.call("mbu_model_add_maxpool", h)
+                elif kind == "concat":
+                    j = index[layer.concat_with]
+                    _lib.call("mbu_model_add_concat", h, j)
+                    shift = segment_lanes(segs)
+                    segs = segs + tuple(ChannelSegment(s.lane_offset + shift, s.count)
+                                        for s in self.out_segments[j])
+                    cur_c = cur_c + self.out_channels[j]
+                else:
+                    raise UnsupportedConfigError(f"unknown layer kind {kind!r}")
+                index[layer.name] = i
+                self.names.append(layer.name)
+                self.kinds.append(kind)
+                self.out_segments.append(segs)
+                self.out_channels.append(cur_c)
+        self._finalizer = weakref.finalize(self, _destroy_model, h)
+        self.planned = None
+        self.ws_bytes = 0
+
+    def plan(self, n, height, width, trace=False):
+        key = (n, height, width, bool(trace))
+        if self.planned == key:
+            return self.ws_bytes
+        size = ctypes.c_size_t()
+        _lib.call("mbu_model_plan", self.handle, n, height, width, int(bool(trace)),
+                  ctypes.byref(size))
+        self.planned = key
+        self.ws_bytes = int(size.value)
+        return self.ws_bytes
+
+    def run(self, image, logits, mask, workspace, path=_lib.PATH_AUTO, stream=None):
+        """Enqueue one forward on ``stream`` (all arguments CUDA tensors)."""
+        s = _stream(self.device) if stream is None else ctypes.c_void_p(stream.cuda_stream)
+        _lib.call("mbu_forward", self.handle, _ptr(image), _ptr(logits), _ptr(mask),
+                  _ptr(workspace), workspace.numel() * workspace.element_size(), path, s)
+
+    def layer_info(self, i):
+        vals = [ctypes.c_int() for _ in range(7)]
+        ob, ab = ctypes.c_size_t(), ctypes.c_size_t()
+        accc = ctypes.c_int()
+        _lib.call("mbu_model_layer_info", self.handle, i, *[ctypes.byref(v) for v in vals],
+                  ctypes.byref(ob), ctypes.byref(ab), ctypes.byref(accc))
+        kind, n, h, w, cw, stride, off = (v.value for v in vals)
+        nofs = ctypes.c_size_t(-1).value
+        return dict(kind=kind, n=n, h=h, w=w, wpp=cw, stride=stride, offset=off,
+                    out_off=None if ob.value == nofs else ob.value,
+                    acc_off=None if ab.value == nofs else ab.value, acc_c=accc.value)
+
+    def read_trace(self, workspace: torch.Tensor, logits_np: np.ndarray) -> dict:
+        """Assemble the reference trace dict from the planned workspace."""
+        ws = workspace.view(torch.uint8)
+        trace = {}
+        for i, name in enumerate(self.names):
+            info = self.layer_info(i)
+            n, h, w = info["n"], info["h"], info["w"]
+            acc = None
+            if info["acc_off"] is not None:
+                c = info["acc_c"]
+                is_f = self.kinds[i] == "float-conv"
+                nbytes = n * h * w * c * (8 if is_f else 4)
+                raw = ws[info["acc_off"]:info["acc_off"] + nbytes]
+                acc = raw.view(torch.float64 if is_f else torch.int32).reshape(n, h, w, c)
+                acc = acc.cpu().numpy()
+            if info["kind"] == 1:  # the head: float logits
+                out = logits_np
+                acc = logits_np
+            else:
+                stride, off, wpp = info["stride"], info["offset"], info["wpp"]
+                nbytes = n * h * w * stride * 8
+                raw = ws[info["out_off"]:info["out_off"] + nbytes].view(torch.int64)
+                words = raw.reshape(n, h, w, stride)[..., off:off + wpp].cpu().numpy()
+                out = BitTensor(n, h, w, self.out_channels[i],
+                                np.ascontiguousarray(words).view(np.uint64),
+                                self.out_segments[i])
+            trace[name] = {"acc": acc, "out": out}
+        return trace
+
+
+def _destroy_model(h):
+    if _lib._lib is not None:
+        _lib.load().mbu_model_destroy(h)
+
+
+_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _device_model(model, device) -> DeviceModel:
+    dev = cuda_device(device)
+    per_model = _CACHE.setdefault(model, {})
+    dm = per_model.get(dev)
+    if dm is None:
+        dm = per_model[dev] = DeviceModel(model, dev)
+    return dm
+
+
+def forward(model, image, threads: int = 1, trace: bool = False, *, device=None,
+            path=_lib.PATH_AUTO):
+    """Run the compiled network on an (n, H, W, C) float64 image, on the GPU."""
+    cfg = model.config
+    image = np.asarray(image, dtype=np.float64)
+    if image.ndim != 4 or image.shape[1:] != (cfg.height, cfg.width, cfg.in_channels):
+        raise ShapeError(
+            f"image shape {image.shape} != (n, {cfg.height}, {cfg.width}, {cfg.in_channels})")
+    dm = _device_model(model, device)
+    n = image.shape[0]
+    dev = dm.device
+    ws_bytes = dm.plan(n, cfg.height, cfg.width, trace)
+    with torch.cuda.device(dev):
+        ws = torch.empty(max(ws_bytes, 8) // 8 + 1, dtype=torch.int64, device=dev)
+        img = torch.from_numpy(np.ascontiguousarray(image)).to(dev)
+        out_c = cfg.out_channels
+        logits = torch.empty((n, cfg.height, cfg.width, out_c), dtype=torch.float64, device=dev)
+        mask = torch.empty((n, cfg.height, cfg.width, out_c), dtype=torch.uint8, device=dev)
+        dm.run(img, logits, mask, ws, path=path)
+        logits_np = logits.cpu().numpy()
+        mask_np = mask.cpu().numpy()
+        notes = None
+        if trace:
+            notes = dm.read_trace(ws, logits_np)
+            notes["mask"] = mask_np
+    return _result_cls()(logits_np, mask_np, notes)
+
+
+class Engine:
+    """Steady-state executor: fixed batch, resident buffers, one CUDA graph.
+
+    ``run()`` replays the captured forward on device-resident inputs;
+    ``run_e2e(host_image, host_logits, host_mask)`` adds the pinned
+    host->device image copy and the device->host logits/mask copies, the
+    way a serving loop would use it.
+    """
+
+    def __init__(self, model, batch: int, device=None, use_graph: bool = True,
+                 path=_lib.PATH_AUTO, with_logits: bool = True):
+        cfg = model.config
+        self.dm = _device_model(model, device)
+        self.device = self.dm.device
+        self.batch = batch
+        self.shape = (batch, cfg.height, cfg.width, cfg.in_channels)
+        self.out_shape = (batch, cfg.height, cfg.width, cfg.out_channels)
+        ws_bytes = self.dm.plan(batch, cfg.height, cfg.width, False)
+        dev = self.device
+        with torch.cuda.device(dev):
+            self.ws = torch.empty(max(ws_bytes, 8) // 8 + 1, dtype=torch.int64, device=dev)
+            self.image = torch.zeros(self.shape, dtype=torch.float64, device=dev)
+            self.logits = torch.empty(self.out_shape, dtype=torch.float64, device=dev)
+            self.mask = torch.empty(self.out_shape, dtype=torch.uint8, device=dev)
+            self.stream = torch.cuda.Stream(dev)
+            self.path = path
+            self.graph = None
+            self.launches_per_run = None
+            before = _lib.launch_count()
+            with torch.cuda.stream(self.stream):
+                self._enqueue()
+            self.stream.synchronize()
+            self.launches_per_run = _lib.launch_count() - before
+            if use_graph:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.stream):
+                    self._enqueue()
+                self.graph = g
+
+    def _enqueue(self):
+        self.dm.run(self.image, self.logits, self.mask, self.ws, path=self.path,
+                    stream=torch.cuda.current_stream(self.device))
+
+    def run(self):
+        with torch.cuda.stream(self.stream):
+            if self.graph is not None:
+                self.graph.replay()
+            else:
+                self._enqueue()
+
+    def run_e2e(self, host_image: torch.Tensor, host_logits: torch.Tensor | None,
+                host_mask: torch.Tensor):
+        with torch.cuda.stream(self.stream):
+            self.image.copy_(host_image, non_blocking=True)
+            if self.graph is not None:
+                self.graph.replay()
+            else:
+                self._enqueue()
+            if host_logits is not None:
+                host_logits.copy_(self.logits, non_blocking=True)
+            host_mask.copy_(self.mask, non_blocking=True)

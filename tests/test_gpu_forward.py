@@ -1,0 +1,144 @@
+"""GPU parity of the whole MBU-Net forward — runs on the B200 box.
+
+* Tiny models (5 precision / pad variants, 16x16 and 32x32): every layer's
+  int32 accumulators and packed output words must equal the reference's
+  golden trace exactly; logits within 1e-9 (the reference's own float
+  tolerance, verify.py:23); masks exact.
+* Config 1 (1x3x256x256, default widths): per-layer SHA-256 of the
+  reference's accumulators / words, logits and mask, for the reference
+  generator and the activation-preserving "live" generator.
+* Size-independent properties at full config-3 shape: CUDA-graph replay ==
+  eager, batch-split invariance, path invariance (tcgen05 vs popcount).
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2601_11660_b200 as mb
+from conftest import load_golden, tiny_config
+from oracle import dense
+from paper_2601_11660_b200 import _lib
+from tests_golden_models import VARIANTS, golden_model, golden_model_256
+
+pytestmark = pytest.mark.gpu
+
+FLOAT_TOL = 1e-9
+
+
+def sha(a) -> str:
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(a.dtype.str.encode() + str(a.shape).encode() + a.tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+@pytest.mark.parametrize("path", [_lib.PATH_AUTO, _lib.PATH_POPCOUNT])
+def test_tiny_forward_matches_reference_trace(cuda, variant, path):
+    z = load_golden("forward_tiny.npz")
+    for extent in (16, 32):
+        key = f"{variant}@{extent}"
+        cfg, bundle, model = golden_model(variant, extent)
+        res = mb.runtime.forward(model, z[f"{key}/image"], trace=True, path=path)
+        assert np.array_equal(res.mask, z[f"{key}/mask"]), key
+        assert np.allclose(res.logits, z[f"{key}/logits"], rtol=FLOAT_TOL, atol=FLOAT_TOL)
+        assert res.trace["head"]["acc"] is res.logits
+        for layer in model.layers:
+            name = layer.name
+            out_key, acc_key = f"{key}/{name}/out", f"{key}/{name}/acc"
+            got = res.trace[name]
+            want_out = z[out_key]
+            if want_out.dtype == np.uint64:
+                assert np.array_equal(got["out"].words, want_out), (key, name)
+            if acc_key in z.files:
+                want = z[acc_key]
+                if np.issubdtype(want.dtype, np.integer):
+                    assert np.array_equal(got["acc"], want), (key, name)
+                else:
+                    assert np.allclose(got["acc"], want, rtol=FLOAT_TOL, atol=FLOAT_TOL), (key, name)
+
+
+@pytest.mark.parametrize("gen,seed", [("synth", 1), ("live", 1), ("live", 2)])
+def test_config1_256_matches_reference(cuda, gen, seed):
+    z = load_golden("forward_256.npz")
+    key = f"{gen}{seed}@256"
+    cfg, bundle, model, image = golden_model_256(gen, seed)
+    res = mb.forward(model, image, trace=True)
+    assert np.allclose(res.logits, z[f"{key}/logits"], rtol=FLOAT_TOL, atol=FLOAT_TOL)
+    assert np.array_equal(res.mask, z[f"{key}/mask"])
+    for layer in model.layers:
+        rec = res.trace[layer.name]
+        k_out, k_acc = f"{key}/{layer.name}/out_sha", f"{key}/{layer.name}/acc_sha"
+        if k_out in z.files:
+            assert sha(rec["out"].words) == bytes(z[k_out]).decode(), layer.name
+        if k_acc in z.files:
+            assert sha(rec["acc"]) == bytes(z[k_acc]).decode(), layer.name
+
+
+def test_forward_vs_dense_oracle_live_64(cuda):
+    for seed in (3, 4):
+        cfg = tiny_config(extent=64, precision=mb.PrecisionMap.from_config_id(seed * 997 % 4096))
+        rng = np.random.default_rng(seed)
+        bundle = mb.live_bundle(cfg, rng)
+        model = mb.build(cfg, bundle)
+        image = rng.random((2, 64, 64, 3))
+        res = mb.forward(model, image, trace=True)
+        ref = dense.ref_forward(cfg, mb.dense_records(mb.quantize_bundle(bundle, cfg), cfg), image)
+        assert np.array_equal(res.mask, ref["mask"])
+        for name, r in ref.items():
+            if name == "mask" or r["acc"] is None:
+                continue
+            if np.issubdtype(np.asarray(r["acc"]).dtype, np.integer):
+                assert np.array_equal(res.trace[name]["acc"], r["acc"]), name
+
+
+def test_reference_model_objects_are_accepted(cuda):
+    # duck typing: only attribute names matter (models from bitunet.build work)
+    cfg, bundle, model = golden_model("all-masked", 16)
+    import types
+
+    layers = tuple(types.SimpleNamespace(**vars(l)) for l in model.layers)
+    alien = types.SimpleNamespace(config=cfg, layers=layers)
+    img = np.random.default_rng(0).random((1, 16, 16, 3))
+    assert np.array_equal(mb.forward(alien, img).mask, mb.forward(model, img).mask)
+
+
+def test_shape_errors(cuda):
+    cfg, bundle, model = golden_model("all-masked", 16)
+    with pytest.raises(mb.ShapeError):
+        mb.forward(model, np.zeros((1, 16, 16, 4)))
+    with pytest.raises(mb.ShapeError):
+        mb.forward(model, np.zeros((16, 16, 3)))
+
+
+def test_engine_graph_replay_and_batch_split_at_config3_shape(cuda):
+    """Full 1024x2048 widths: graph == eager; batch of 2 == two batches of 1."""
+    cfg = mb.UNetConfig(height=1024, width=2048)
+    rng = np.random.default_rng(11)
+    model = mb.build(cfg, mb.live_bundle(cfg, rng))
+    img = torch.from_numpy(rng.random((2, 1024, 2048, 3))).to(cuda)
+    eng = mb.Engine(model, batch=2)
+    eng.image.copy_(img)
+    eng.run()
+    torch.cuda.synchronize()
+    mask2, logits2 = eng.mask.clone(), eng.logits.clone()
+    eng1 = mb.Engine(model, batch=1, use_graph=False)
+    for i in range(2):
+        eng1.image.copy_(img[i:i + 1])
+        eng1.run()
+        torch.cuda.synchronize()
+        assert torch.equal(eng1.mask, mask2[i:i + 1])
+        assert torch.equal(eng1.logits, logits2[i:i + 1])
+    m = mask2.float().mean().item()
+    assert 0.02 < m < 0.98, m  # live generator: a non-trivial mask
+
+
+def test_path_invariance_at_256(cuda):
+    cfg, bundle, model, image = golden_model_256("live", 1)
+    a = mb.runtime.forward(model, image, path=_lib.PATH_AUTO)
+    b = mb.runtime.forward(model, image, path=_lib.PATH_POPCOUNT)
+    assert np.array_equal(a.mask, b.mask)
+    assert np.array_equal(a.logits, b.logits)
