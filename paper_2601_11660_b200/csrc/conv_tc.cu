@@ -1,13 +1,527 @@
-// tcgen05 implicit-GEMM conv (placeholder until the UTCIMMA kernel lands).
+// Masked-binary convolution as a tcgen05 (UTCIMMA) implicit GEMM, sm_100a.
+//
+// Replaces conv_forward -> lower_conv_to_gemm -> bit_gemm ->
+// xor_popcount_rows + apply_threshold (layers.py:258-313, :508-522,
+// bitcore.py:265-294, kernels.py:82-91) and, with TAPS = 1 and a scatter
+// epilogue, transposed_conv_forward (layers.py:316-352).
+//
+// Arithmetic. The reference computes, per output (pixel m, channel o),
+//   masked: popc(a'^neg) - popc(a'^pos)      binary: k_true - 2 popc(a'^b')
+// over packed lanes. Both equal the integer dot product
+//   acc = sum_lanes a * w,  a = 2a'-1 in {-1,+1},  w in {-1,0,+1}
+// where w = pos - neg (masked) or 2b'-1 on real lanes and 0 on pad lanes
+// (binary). This kernel evaluates exactly that sum on the 5th-gen tensor
+// cores with kind::i8 (s8 x s8 -> s32): weights are expanded once at upload
+// into s8, activations stay bit-packed in HBM and are expanded to s8 +-1 in
+// shared memory by producer warps. |acc| <= 9*c_in < 2^31: exact.
+// Out-of-bounds taps read -1 (pad_mode "neg_one", the zero-word gather of
+// layers.py:270) or 0 (pad_mode "zero", equal to the reference's
+// weight-sum correction, layers.py:306-312).
+//
+// Implicit GEMM without im2col: a CTA expands a halo'd strip of input rows
+// (R+2 rows x TW+2 columns) ONCE per 32-channel chunk; the A operand of tap
+// (dy, dx) is the same strip with the UMMA descriptor's start address moved
+// by (dy-1)*P + (dx-1) rows of 16 B (K-major, no swizzle: a row is 16 B, so
+// any pixel offset is a legal start). Nine MMAs per chunk read one strip.
+//
+// Roles (192 threads): warps 0-3 expand bits -> s8 strips (producers), then
+// drain TMEM through the fused threshold + bit-pack epilogue; warp 4 (one
+// lane) issues tcgen05.mma; warp 5 (one lane) streams the pre-arranged
+// weight stage with cp.async.bulk. Stages are recycled through mbarriers
+// (full: 128 producer arrivals + TMA tx bytes; empty: tcgen05.commit).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
 #include "common.cuh"
+
 namespace mbu {
-int prepare_conv_tc(mbu_conv *cv, const uint64_t *, const uint64_t *, const int32_t *,
-                    const int32_t *, int) {
+namespace tc {
+
+constexpr int BLOCK_M = 128;
+constexpr int NUM_PRODUCER_WARPS = 4;
+constexpr int MMA_WARP = 4;
+constexpr int BLOAD_WARP = 5;
+constexpr int NUM_THREADS = 192;
+constexpr int TMEM_COLS = 256;
+constexpr int MAX_STAGES = 4;
+constexpr int SMEM_HEADER = 1024;
+
+struct Params {
+  const uint32_t *x32;
+  int n, h, w;              // A pixel grid (conv: = output grid)
+  int x_stride32, x_off32;
+  int halo, P, Q, R, TW, row_mode, MB;
+  int col_tiles, row_tiles, n_tiles;
+  int zero_pad;
+  int kc;
+  const int32_t *chunk_word;
+  const int8_t *b;
+  int n_tile;
+  uint32_t b_stage_bytes, a_stage_bytes;
+  uint32_t idesc;
+  int stages;
+  int c_out, c_out_pad, n_gemm;
+  int tconv_s;              // 0 for conv
+  int ho, wo;
+  int32_t *acc;
+  uint32_t *bits;
+  int out_stride32, out_off32, out_groups;
+  const int32_t *thr;
+  const uint8_t *codes;
+};
+
+// ----------------------------------------------------------------- PTX glue
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// UMMA shared-memory descriptor: K-major, SWIZZLE_NONE, sm100 version 1.
+// Canonical layout ((8,m),(16B,2)) : ((16B, SBO), (1, LBO)).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = uint64_t((saddr >> 4) & 0x3FFFu);
+  d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
+  d |= uint64_t(1) << 46;
+  return d;
+}
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// 4 activation bits -> 4 s8 lanes of +-1 (bit 1 -> 0x01, bit 0 -> 0xFF)
+__device__ __forceinline__ uint32_t expand4(uint32_t nib) {
+  const uint32_t spread = (nib * 0x00204081u) & 0x01010101u;
+  return ~(spread * 0xFEu);
+}
+__device__ __forceinline__ void expand32(uint32_t b, uint4 &lo, uint4 &hi) {
+  lo.x = expand4(b & 0xF);
+  lo.y = expand4((b >> 4) & 0xF);
+  lo.z = expand4((b >> 8) & 0xF);
+  lo.w = expand4((b >> 12) & 0xF);
+  hi.x = expand4((b >> 16) & 0xF);
+  hi.y = expand4((b >> 20) & 0xF);
+  hi.z = expand4((b >> 24) & 0xF);
+  hi.w = expand4(b >> 28);
+}
+__device__ __forceinline__ void sts128(uint32_t addr, const uint4 &v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ int block_q0(const Params &p, int b) {
+  return p.row_mode ? (b + p.halo) * p.P + p.halo : p.halo * p.P + p.halo + BLOCK_M * b;
+}
+
+// ------------------------------------------------------------------ kernel
+template <int TAPS, bool TCONV>
+__global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+  uint64_t *empty = full + MAX_STAGES;
+  uint64_t *done = empty + MAX_STAGES;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+  uint8_t *a_base = smem + SMEM_HEADER;
+  uint8_t *b_base = a_base + size_t(p.stages) * p.a_stage_bytes;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  int t = blockIdx.x;
+  const int nt = t % p.n_tiles;
+  t /= p.n_tiles;
+  const int ct = t % p.col_tiles;
+  t /= p.col_tiles;
+  const int rt = t % p.row_tiles;
+  const int nb = t / p.row_tiles;
+  const int y0 = rt * p.R;
+  const int x0 = ct * p.TW;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(smem_u32(&full[s]), NUM_PRODUCER_WARPS * 32 + 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    mbar_init(smem_u32(done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int S = p.stages;
+
+  if (warp < NUM_PRODUCER_WARPS) {
+    // ---------------- producers: packed bits -> s8 strips
+    const uint32_t oob_word = p.zero_pad ? 0u : 0xFFFFFFFFu;
+    const uint4 oob = make_uint4(oob_word, oob_word, oob_word, oob_word);
+    const int strip_rows = p.R + 2 * p.halo;
+    for (int k = 0; k < p.kc; ++k) {
+      const int s = k % S;
+      const int u = k / S;
+      if (u > 0) mbar_wait(smem_u32(&empty[s]), (u - 1) & 1);
+      const uint32_t a0 = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
+      const uint32_t a1 = a0 + p.Q * 16;
+      const int cw = __ldg(p.chunk_word + k);
+      for (int q = threadIdx.x; q < p.Q; q += NUM_PRODUCER_WARPS * 32) {
+        const int rr = q / p.P;
+        const int cc = q - rr * p.P;
+        const int iy = y0 - p.halo + rr;
+        const int ix = x0 - p.halo + cc;
+        uint4 lo = oob, hi = oob;
+        if (rr < strip_rows && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w) {
+          const int64_t pix = (int64_t(nb) * p.h + iy) * p.w + ix;
+          const uint32_t bitsw = __ldg(p.x32 + pix * p.x_stride32 + p.x_off32 + cw);
+          expand32(bitsw, lo, hi);
+        }
+        sts128(a0 + q * 16, lo);
+        sts128(a1 + q * 16, hi);
+      }
+      fence_proxy_async();
+      mbar_arrive(smem_u32(&full[s]));
+    }
+
+    // ---------------- epilogue: TMEM -> threshold -> packed bits / int32 acc
+    mbar_wait(smem_u32(done), 0);
+    tc_fence_after();
+    const int m = warp * 32 + lane;
+    const uint32_t lane_addr = tmem + (uint32_t(warp * 32) << 16);
+    const int groups = p.n_tile / 32;
+    for (int b = 0; b < p.MB; ++b) {
+      const int q = block_q0(p, b) + m;
+      const int r = q / p.P - p.halo;
+      const int c = q % p.P - p.halo;
+      const int yy = y0 + r, xx = x0 + c;
+      const bool valid = r >= 0 && r < p.R && c >= 0 && c < p.TW && yy < p.h && xx < p.w;
+      for (int g = 0; g < groups; ++g) {
+        uint32_t v[32];
+        tmem_ld32(lane_addr + uint32_t(b * p.n_tile + g * 32), v);
+        const int j0 = nt * p.n_tile + g * 32;
+        if (!valid || j0 >= p.n_gemm) continue;
+        int o0, oy, ox;
+        if (TCONV) {
+          const int tap = j0 / p.c_out_pad;
+          o0 = j0 - tap * p.c_out_pad;
+          oy = yy * p.tconv_s + tap / p.tconv_s;
+          ox = xx * p.tconv_s + tap % p.tconv_s;
+        } else {
+          o0 = j0;
+          oy = yy;
+          ox = xx;
+        }
+        const int64_t opix = (int64_t(nb) * p.ho + oy) * p.wo + ox;
+        if (p.bits) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            word |= uint32_t(fires(int(v[i]), __ldg(p.thr + o0 + i), __ldg(p.codes + o0 + i))) << i;
+          uint32_t *dst = p.bits + opix * p.out_stride32 + p.out_off32;
+          dst[o0 / 32] = word;
+          if (o0 / 32 == p.c_out_pad / 32 - 1)
+            for (int gg = p.c_out_pad / 32; gg < p.out_groups; ++gg) dst[gg] = 0u;
+        }
+        if (p.acc) {
+          int32_t *dst = p.acc + opix * p.c_out + o0;
+          if (o0 + 32 <= p.c_out && (p.c_out % 4) == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              *reinterpret_cast<int4 *>(dst + i) =
+                  make_int4(int(v[i]), int(v[i + 1]), int(v[i + 2]), int(v[i + 3]));
+          } else {
+            for (int i = 0; i < 32 && o0 + i < p.c_out; ++i) dst[i] = int(v[i]);
+          }
+        }
+      }
+    }
+  } else if (warp == MMA_WARP) {
+    // ---------------- single-thread MMA issue
+    if (lane == 0) {
+      const uint32_t sbo = 128;
+      const uint32_t a_lbo = uint32_t(p.Q) * 16;
+      const uint32_t b_lbo = uint32_t(p.n_tile) * 16;
+      for (int k = 0; k < p.kc; ++k) {
+        const int s = k % S;
+        mbar_wait(smem_u32(&full[s]), (k / S) & 1);
+        tc_fence_after();
+        const uint32_t a_s = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
+        const uint32_t b_s = smem_u32(b_base + size_t(s) * p.b_stage_bytes);
+        for (int b = 0; b < p.MB; ++b) {
+          const int q0 = block_q0(p, b);
+#pragma unroll
+          for (int tap = 0; tap < TAPS; ++tap) {
+            const int off = TAPS == 9 ? (tap / 3 - 1) * p.P + (tap % 3 - 1) : 0;
+            const uint64_t ad = umma_desc(a_s + uint32_t(q0 + off) * 16, a_lbo, sbo);
+            const uint64_t bd = umma_desc(b_s + uint32_t(tap * p.n_tile * 32), b_lbo, sbo);
+            umma_i8(tmem + uint32_t(b * p.n_tile), ad, bd, p.idesc, (k | tap) != 0);
+          }
+        }
+        umma_commit(smem_u32(&empty[s]));
+      }
+      umma_commit(smem_u32(done));
+    }
+    __syncwarp();
+  } else if (warp == BLOAD_WARP) {
+    // ---------------- weight stages: one bulk copy per stage
+    if (lane == 0) {
+      const int8_t *src = p.b + size_t(nt) * p.kc * p.b_stage_bytes;
+      for (int k = 0; k < p.kc; ++k) {
+        const int s = k % S;
+        const int u = k / S;
+        if (u > 0) mbar_wait(smem_u32(&empty[s]), (u - 1) & 1);
+        const uint32_t bar = smem_u32(&full[s]);
+        mbar_arrive_expect_tx(bar, p.b_stage_bytes);
+        bulk_g2s(smem_u32(b_base + size_t(s) * p.b_stage_bytes), src + size_t(k) * p.b_stage_bytes,
+                 p.b_stage_bytes, bar);
+      }
+    }
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+}  // namespace tc
+
+// --------------------------------------------------------------------------
+// host side: eligibility, weight repack, launch geometry
+// --------------------------------------------------------------------------
+int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, const int32_t *seg_off,
+                    const int32_t *seg_cnt, int n_seg) {
   cv->tc_ok = 0;
+  const bool conv3 = !cv->transposed && cv->kh == 3 && cv->kw == 3 && cv->stride == 1 && cv->pad == 1;
+  const bool conv1 = !cv->transposed && cv->kh == 1 && cv->kw == 1 && cv->stride == 1 && cv->pad == 0;
+  const bool tconv = cv->transposed && cv->stride <= 4;
+  if (!(conv3 || conv1 || tconv)) return MBU_OK;
+  const int lpp = cv->lpp;
+  const int n_chunks = lpp / 32;
+  std::vector<uint8_t> real(lpp, 0);
+  for (int i = 0; i < n_seg; ++i)
+    for (int l = seg_off[i]; l < seg_off[i] + seg_cnt[i]; ++l) real[l] = 1;
+  std::vector<int32_t> chunk_word;
+  for (int c = 0; c < n_chunks; ++c) {
+    bool any = false;
+    for (int l = 32 * c; l < 32 * c + 32; ++l) any |= real[l] != 0;
+    if (any) chunk_word.push_back(c);
+  }
+  const int kc = int(chunk_word.size());
+  if (kc == 0) return MBU_OK;
+  const int taps = cv->transposed ? 1 : cv->kh * cv->kw;
+  const int s2 = cv->transposed ? cv->stride * cv->stride : 1;
+  const int c_out_pad = (cv->c_out + 31) / 32 * 32;
+  const int n_gemm = s2 * c_out_pad;
+  const int n_tile = n_gemm <= 128 ? n_gemm : 128;
+  const int n_tiles = (n_gemm + n_tile - 1) / n_tile;
+  const size_t b_stage = size_t(taps) * n_tile * 32;
+  std::vector<int8_t> b(size_t(n_tiles) * kc * b_stage, 0);
+  const int ptaps = cv->kh * cv->kw;  // taps in the reference plane layout
+  const size_t row_words = size_t(ptaps) * cv->wpp;
+  auto bit = [&](const uint64_t *plane, int o, int tap, int L) -> int {
+    return int((plane[size_t(o) * row_words + size_t(tap) * cv->wpp + (L >> 6)] >> (L & 63)) & 1ull);
+  };
+  for (int nt = 0; nt < n_tiles; ++nt)
+    for (int k = 0; k < kc; ++k)
+      for (int tap = 0; tap < taps; ++tap)
+        for (int half = 0; half < 2; ++half)
+          for (int n = 0; n < n_tile; ++n) {
+            const int j = nt * n_tile + n;
+            if (j >= n_gemm) continue;
+            int o = j, ptap = tap;
+            if (cv->transposed) {
+              ptap = j / c_out_pad;
+              o = j % c_out_pad;
+            }
+            if (o >= cv->c_out) continue;
+            int8_t *dst = &b[((size_t(nt) * kc + k) * taps + tap) * n_tile * 32 + size_t(half) * n_tile * 16 +
+                             size_t(n) * 16];
+            for (int i = 0; i < 16; ++i) {
+              const int L = 32 * chunk_word[k] + 16 * half + i;
+              int v;
+              if (neg) v = bit(pos, o, ptap, L) - bit(neg, o, ptap, L);
+              else v = real[L] ? 2 * bit(pos, o, ptap, L) - 1 : 0;
+              dst[i] = int8_t(v);
+            }
+          }
+  MBU_TRY(check_cuda(cudaMalloc(&cv->d_b, b.size()), "alloc tc weights"));
+  MBU_TRY(check_cuda(cudaMemcpy(cv->d_b, b.data(), b.size(), cudaMemcpyHostToDevice), "upload tc weights"));
+  MBU_TRY(check_cuda(cudaMalloc(&cv->d_chunk_word, kc * sizeof(int32_t)), "alloc chunk map"));
+  MBU_TRY(check_cuda(cudaMemcpy(cv->d_chunk_word, chunk_word.data(), kc * sizeof(int32_t),
+                                cudaMemcpyHostToDevice),
+                     "upload chunk map"));
+  cv->taps = taps;
+  cv->kc = kc;
+  cv->n_gemm = n_gemm;
+  cv->n_pad = n_gemm;
+  cv->c_out_pad = c_out_pad;
+  cv->n_tile = n_tile;
+  cv->n_tiles = n_tiles;
+  cv->b_stage_bytes = b_stage;
+  cv->tc_ok = 1;
   return MBU_OK;
 }
-int launch_conv_tc(const mbu_conv *, const ActView &, int, int, int32_t *, uint64_t *, int, int,
-                   cudaStream_t) {
-  return fail(MBU_ERR_UNSUPPORTED, "tcgen05 path not built");
+
+template <int TAPS, bool TCONV>
+static int launch_tc_impl(const tc::Params &p, int grid, size_t smem, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    MBU_TRY(check_cuda(cudaFuncSetAttribute(tc::conv_tc_kernel<TAPS, TCONV>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+                       "cudaFuncSetAttribute"));
+    configured = true;
+  }
+  tc::conv_tc_kernel<TAPS, TCONV><<<grid, tc::NUM_THREADS, smem, st>>>(p);
+  return check_launch("conv_tc_kernel");
 }
+
+int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
+                   uint64_t *bits, int out_stride, int out_offset, cudaStream_t st) {
+  tc::Params p{};
+  p.x32 = reinterpret_cast<const uint32_t *>(x.base);
+  p.n = x.n;
+  p.h = x.h;
+  p.w = x.w;
+  p.x_stride32 = x.stride * 2;
+  p.x_off32 = x.offset * 2;
+  p.halo = cv->taps == 9 ? 1 : 0;
+  p.n_tile = cv->n_tile;
+  p.n_tiles = cv->n_tiles;
+  p.MB = std::min(8, tc::TMEM_COLS / cv->n_tile);
+  if (x.w >= 128) {
+    p.row_mode = 1;
+    p.TW = 128;
+    p.P = 128 + 2 * p.halo;
+    p.R = p.MB;
+    p.col_tiles = (x.w + 127) / 128;
+  } else {
+    p.row_mode = 0;
+    p.TW = x.w;
+    p.P = x.w + 2 * p.halo;
+    p.R = std::max(1, std::min(x.h, (tc::BLOCK_M * p.MB - p.TW) / p.P + 1));
+    p.MB = ((p.R - 1) * p.P + p.TW + tc::BLOCK_M - 1) / tc::BLOCK_M;
+    p.col_tiles = 1;
+  }
+  p.row_tiles = (x.h + p.R - 1) / p.R;
+  const int q_last = p.row_mode ? (p.MB - 1 + p.halo) * p.P + p.halo
+                                : p.halo * p.P + p.halo + tc::BLOCK_M * (p.MB - 1);
+  int Q = q_last + tc::BLOCK_M + (p.halo ? p.P + 1 : 0);
+  Q = std::max(Q, (p.R + 2 * p.halo) * p.P);
+  Q = (Q + 7) / 8 * 8;
+  p.Q = Q;
+  p.a_stage_bytes = uint32_t((size_t(Q) * 32 + 1023) / 1024 * 1024);
+  p.b_stage_bytes = uint32_t(cv->b_stage_bytes);
+  const size_t stage = size_t(p.a_stage_bytes) + p.b_stage_bytes;
+  int stages = int((113 * 1024 - tc::SMEM_HEADER) / stage);
+  if (stages < 2) stages = int((227 * 1024 - tc::SMEM_HEADER) / stage);
+  if (stages < 2) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv stage does not fit in shared memory");
+  p.stages = std::min(stages, tc::MAX_STAGES);
+  p.zero_pad = cv->pad_mode == MBU_PAD_ZERO;
+  p.kc = cv->kc;
+  p.chunk_word = cv->d_chunk_word;
+  p.b = cv->d_b;
+  // instruction descriptor: s32 accum, s8 x s8, K-major both, N, M = 128
+  p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(cv->n_tile >> 3) << 17) |
+            (uint32_t(tc::BLOCK_M >> 4) << 24);
+  p.c_out = cv->c_out;
+  p.c_out_pad = cv->c_out_pad;
+  p.n_gemm = cv->n_gemm;
+  p.tconv_s = cv->transposed ? cv->stride : 0;
+  p.ho = ho;
+  p.wo = wo;
+  p.acc = acc;
+  p.bits = reinterpret_cast<uint32_t *>(bits);
+  p.out_stride32 = out_stride * 2;
+  p.out_off32 = out_offset * 2;
+  p.out_groups = cv->out_wpp * 2;
+  p.thr = cv->d_thr;
+  p.codes = cv->d_codes;
+  const int64_t grid = int64_t(x.n) * p.row_tiles * p.col_tiles * p.n_tiles;
+  if (grid == 0) return MBU_OK;
+  if (grid > 0x7FFFFFFF) return fail(MBU_ERR_SHAPE, "tcgen05 conv grid too large");
+  const size_t smem = tc::SMEM_HEADER + size_t(p.stages) * stage;
+  if (cv->transposed) return launch_tc_impl<1, true>(p, int(grid), smem, st);
+  if (cv->taps == 9) return launch_tc_impl<9, false>(p, int(grid), smem, st);
+  return launch_tc_impl<1, false>(p, int(grid), smem, st);
+}
+
 }  // namespace mbu

@@ -160,11 +160,15 @@ def _destroy_model(h):
 
 
 _CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_STRONG: dict = {}
 
 
 def _device_model(model, device) -> DeviceModel:
     dev = cuda_device(device)
-    per_model = _CACHE.setdefault(model, {})
+    try:
+        per_model = _CACHE.setdefault(model, {})
+    except TypeError:  # not weak-referenceable: keep the model alive with its upload
+        per_model = _STRONG.setdefault(id(model), (model, {}))[1]
     dm = per_model.get(dev)
     if dm is None:
         dm = per_model[dev] = DeviceModel(model, dev)
