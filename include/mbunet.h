@@ -170,6 +170,13 @@ int mbu_model_layer_info(mbu_model *model, int layer, int *out_kind, int *n,
                          int *word_offset, size_t *out_byte_offset,
                          size_t *acc_byte_offset, int *acc_channels);
 
+/* Per-layer timing (measurement only): when enabled, mbu_forward records a
+ * CUDA event on its stream before every layer and after the last one;
+ * mbu_model_layer_times waits for the last event and writes one duration
+ * (ms) per layer. Leave disabled while capturing a CUDA graph. */
+int mbu_model_set_timing(mbu_model *model, int enable);
+int mbu_model_layer_times(mbu_model *model, float *ms_out);
+
 #ifdef __cplusplus
 }
 #endif

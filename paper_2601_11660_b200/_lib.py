@@ -52,6 +52,8 @@ _SIGS = {
     "mbu_model_add_concat": (_i, [_vp, _i]),
     "mbu_model_plan": (_i, [_vp, _i, _i, _i, _i, _c.POINTER(_sz)]),
     "mbu_forward": (_i, [_vp, _vp, _vp, _vp, _vp, _sz, _i, _vp]),
+    "mbu_model_set_timing": (_i, [_vp, _i]),
+    "mbu_model_layer_times": (_i, [_vp, _c.POINTER(_c.c_float)]),
     "mbu_model_layer_info": (_i, [_vp, _i] + [_c.POINTER(_i)] * 7
                              + [_c.POINTER(_sz), _c.POINTER(_sz), _c.POINTER(_i)]),
 }

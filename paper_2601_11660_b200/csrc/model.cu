@@ -43,6 +43,9 @@ struct mbu_model {
   int planned = 0, n = 0, H = 0, W = 0, trace = 0, in_c = 0;
   std::vector<size_t> buf_off, buf_bytes;
   size_t ws = 0;
+  // optional per-layer CUDA-event timing (bench.py roofline)
+  int timing = 0;
+  std::vector<cudaEvent_t> events;  // layers + 1
 };
 
 static int add_buf(mbu_model *m, size_t bytes) {
@@ -64,6 +67,7 @@ int mbu_model_create(mbu_model **out, int device) {
 
 int mbu_model_destroy(mbu_model *m) {
   if (!m) return MBU_OK;
+  for (auto e : m->events) cudaEventDestroy(e);
   for (auto &l : m->layers) {
     mbu_conv_destroy(l.conv);
     mbu_fconv_destroy(l.fconv);
@@ -217,8 +221,10 @@ int mbu_forward(mbu_model *m, const double *image, double *logits, uint8_t *mask
     return ActView{reinterpret_cast<const uint64_t *>(base + m->buf_off[l.buf]), l.n, l.h, l.w,
                    l.wpp, l.stride, l.offset};
   };
+  const bool timed = m->timing && int(m->events.size()) == int(m->layers.size()) + 1;
   for (int i = 0; i < int(m->layers.size()); ++i) {
     const Layer &l = m->layers[i];
+    if (timed) MBU_TRY(check_cuda(cudaEventRecord(m->events[i], st), "cudaEventRecord"));
     uint64_t *out = l.out_kind == 0 ? reinterpret_cast<uint64_t *>(base + m->buf_off[l.buf]) : nullptr;
     void *acc = l.acc_buf >= 0 ? base + m->buf_off[l.acc_buf] : nullptr;
     int in_h = l.src < 0 ? m->H : m->layers[l.src].h;
@@ -247,6 +253,25 @@ int mbu_forward(mbu_model *m, const double *image, double *logits, uint8_t *mask
         break;  // concat: resolved at plan time
     }
   }
+  if (timed) MBU_TRY(check_cuda(cudaEventRecord(m->events.back(), st), "cudaEventRecord"));
+  return MBU_OK;
+}
+
+int mbu_model_set_timing(mbu_model *m, int enable) {
+  if (enable && m->events.size() != m->layers.size() + 1) {
+    for (auto e : m->events) cudaEventDestroy(e);
+    m->events.assign(m->layers.size() + 1, nullptr);
+    for (auto &e : m->events) MBU_TRY(check_cuda(cudaEventCreate(&e), "cudaEventCreate"));
+  }
+  m->timing = enable;
+  return MBU_OK;
+}
+
+int mbu_model_layer_times(mbu_model *m, float *ms_out) {
+  if (m->events.size() != m->layers.size() + 1) return fail(MBU_ERR_ENGINE, "timing not enabled");
+  MBU_TRY(check_cuda(cudaEventSynchronize(m->events.back()), "cudaEventSynchronize"));
+  for (size_t i = 0; i + 1 < m->events.size(); ++i)
+    MBU_TRY(check_cuda(cudaEventElapsedTime(&ms_out[i], m->events[i], m->events[i + 1]), "cudaEventElapsedTime"));
   return MBU_OK;
 }
 

@@ -112,6 +112,16 @@ class DeviceModel:
         _lib.call("mbu_forward", self.handle, _ptr(image), _ptr(logits), _ptr(mask),
                   _ptr(workspace), workspace.numel() * workspace.element_size(), path, s)
 
+    def set_timing(self, enable: bool):
+        """Record CUDA events around every layer of the next eager runs."""
+        _lib.call("mbu_model_set_timing", self.handle, int(bool(enable)))
+
+    def layer_times(self):
+        """Per-layer durations (ms) of the last timed forward, on its stream."""
+        out = (ctypes.c_float * len(self.names))()
+        _lib.call("mbu_model_layer_times", self.handle, out)
+        return list(out)
+
     def layer_info(self, i):
         vals = [ctypes.c_int() for _ in range(7)]
         ob, ab = ctypes.c_size_t(), ctypes.c_size_t()
