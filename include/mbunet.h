@@ -60,6 +60,12 @@ int mbu_version(void);
 int64_t mbu_launch_count(void);
 /* Return the path the last mbu_conv_run / mbu_tconv_run executed. */
 int mbu_last_path(void);
+/* Process-wide switches for cross-checking fast paths against exact ones.
+ * MBU_OPT_GENERIC_ENDPOINTS: 1 = run stem/head through the all-float64
+ * generic kernels instead of the float32-with-exact-recheck stem and the
+ * specialised head (results must be identical). */
+enum { MBU_OPT_GENERIC_ENDPOINTS = 1 };
+int mbu_set_option(int option, int value);
 
 /* ------------------------------------------------------------------ */
 /* Masked-binary / binary convolution (layers.py:289-313 conv_forward, */

@@ -21,6 +21,7 @@ void set_error(const std::string &msg);
 int fail(int status, const std::string &msg);
 extern std::atomic<int64_t> g_launches;
 extern int g_last_path;
+extern int g_force_generic_fconv;  // mbu_set_option(MBU_OPT_GENERIC_ENDPOINTS)
 
 inline int check_launch(const char *what) {
   cudaError_t e = cudaGetLastError();
@@ -92,6 +93,7 @@ struct mbu_conv {
   int n_stages_k = 0;            // K stages per tile (= ceil(kc / chunks_per_stage))
   int32_t *d_chunk_word = nullptr;  // [kc] u32 index inside a pixel for each chunk
   int8_t *d_b = nullptr;         // repacked s8 weights, UMMA K-major core-matrix order
+  void *d_thr2 = nullptr;        // int2 per GEMM column: bit = (m * acc >= t)
   size_t b_stage_bytes = 0;      // bytes of B per (n tile, K stage)
 };
 
@@ -103,6 +105,8 @@ struct mbu_fconv {
   double *d_bias = nullptr;
   double *d_bn = nullptr;     // gamma, beta, mean, sigma (4*c_out)
   int32_t *d_lanes = nullptr; // input lane per channel (bits input)
+  int stem_fast = 0;          // float32 + exact-recheck stem kernel usable
+  void *d_stem = nullptr;     // StemConsts (endpoints.cu)
 };
 
 namespace mbu {
@@ -120,4 +124,9 @@ int launch_fconv(const mbu_fconv *fc, const double *x_f64, const ActView &xb, in
                  uint8_t *mask, cudaStream_t st);
 int conv_run(mbu_conv *cv, const ActView &x, int32_t *acc, uint64_t *bits, int out_stride,
              int out_offset, int path, cudaStream_t st);
+int stem_prepare(mbu_fconv *fc, const double *w, const double *bias, const double *bn, double eps);
+int launch_stem_fast(const mbu_fconv *fc, const double *x, int n, int h, int w, uint64_t *bits,
+                     int out_stride, int out_offset, cudaStream_t st);
+int launch_head_fast(const mbu_fconv *fc, const ActView &xb, int n, int h, int w, double *logits,
+                     uint8_t *mask, cudaStream_t st);
 }  // namespace mbu

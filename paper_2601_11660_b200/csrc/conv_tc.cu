@@ -1,4 +1,4 @@
-// Masked-binary convolution as a tcgen05 (UTCIMMA) implicit GEMM, sm_100a.
+// Masked-binary convolution as a persistent tcgen05 (UTCIMMA) implicit GEMM.
 //
 // Replaces conv_forward -> lower_conv_to_gemm -> bit_gemm ->
 // xor_popcount_rows + apply_threshold (layers.py:258-313, :508-522,
@@ -11,24 +11,28 @@
 //   acc = sum_lanes a * w,  a = 2a'-1 in {-1,+1},  w in {-1,0,+1}
 // where w = pos - neg (masked) or 2b'-1 on real lanes and 0 on pad lanes
 // (binary). This kernel evaluates exactly that sum on the 5th-gen tensor
-// cores with kind::i8 (s8 x s8 -> s32): weights are expanded once at upload
-// into s8, activations stay bit-packed in HBM and are expanded to s8 +-1 in
-// shared memory by producer warps. |acc| <= 9*c_in < 2^31: exact.
+// cores with kind::i8 (s8 x s8 -> s32 in TMEM): weights are expanded once at
+// upload into s8, activations stay bit-packed in HBM and are expanded to s8
+// +-1 in shared memory by producer warps. |acc| <= 9*c_in < 2^31: exact.
 // Out-of-bounds taps read -1 (pad_mode "neg_one", the zero-word gather of
-// layers.py:270) or 0 (pad_mode "zero", equal to the reference's
-// weight-sum correction, layers.py:306-312).
+// layers.py:270) or 0 (pad_mode "zero", equal to the reference's weight-sum
+// correction, layers.py:306-312).
 //
-// Implicit GEMM without im2col: a CTA expands a halo'd strip of input rows
-// (R+2 rows x TW+2 columns) ONCE per 32-channel chunk; the A operand of tap
-// (dy, dx) is the same strip with the UMMA descriptor's start address moved
-// by (dy-1)*P + (dx-1) rows of 16 B (K-major, no swizzle: a row is 16 B, so
-// any pixel offset is a legal start). Nine MMAs per chunk read one strip.
+// Implicit GEMM without im2col: the producers expand a halo'd strip of input
+// rows (R+2 rows x TW+2 columns) ONCE per 32-channel chunk; the A operand of
+// tap (dy, dx) is that same strip with the UMMA descriptor's start address
+// moved by (dy-1)*P + (dx-1) rows of 16 B (K-major, no swizzle: one row is
+// 16 B, so any pixel offset is a legal start). Nine MMAs read one strip.
 //
-// Roles (192 threads): warps 0-3 expand bits -> s8 strips (producers), then
-// drain TMEM through the fused threshold + bit-pack epilogue; warp 4 (one
-// lane) issues tcgen05.mma; warp 5 (one lane) streams the pre-arranged
-// weight stage with cp.async.bulk. Stages are recycled through mbarriers
-// (full: 128 producer arrivals + TMA tx bytes; empty: tcgen05.commit).
+// Persistent, warp-specialised (512 threads, one CTA per SM):
+//   warps 0-7   epilogue: TMEM -> fused threshold + bit-pack -> HBM
+//               (warp w drains TMEM lanes 32*(w%4).. of M-blocks b = w/4 mod 2)
+//   warps 8-13  producers: packed bits -> s8 strips (batched loads)
+//   warp 14     one lane issues tcgen05.mma; owns TMEM alloc/dealloc
+//   warp 15     one lane streams pre-arranged weight stages (cp.async.bulk)
+// Smem stages cycle through full/empty mbarriers; two TMEM accumulator
+// buffers (2 x 256 columns) let the epilogue of tile i overlap the MMAs of
+// tile i+1.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -41,20 +45,28 @@ namespace mbu {
 namespace tc {
 
 constexpr int BLOCK_M = 128;
-constexpr int NUM_PRODUCER_WARPS = 4;
-constexpr int MMA_WARP = 4;
-constexpr int BLOAD_WARP = 5;
-constexpr int NUM_THREADS = 192;
-constexpr int TMEM_COLS = 256;
-constexpr int MAX_STAGES = 4;
+constexpr int NUM_EPI_WARPS = 8;
+constexpr int NUM_PROD_WARPS = 6;
+constexpr int PROD_WARP0 = NUM_EPI_WARPS;
+constexpr int MMA_WARP = PROD_WARP0 + NUM_PROD_WARPS;
+constexpr int BLOAD_WARP = MMA_WARP + 1;
+constexpr int NUM_THREADS = (BLOAD_WARP + 1) * 32;
+constexpr int PROD_THREADS = NUM_PROD_WARPS * 32;
+constexpr int EPI_THREADS = NUM_EPI_WARPS * 32;
+constexpr int ACC_COLS = 256;   // one accumulator buffer
+constexpr int TMEM_COLS = 512;  // two buffers
+constexpr int MAX_STAGES = 8;
 constexpr int SMEM_HEADER = 1024;
+constexpr int MIN_SMEM = 120 * 1024;  // > half an SM: exactly one CTA (and TMEM owner) per SM
+constexpr int UNROLL = 4;
 
 struct Params {
   const uint32_t *x32;
   int n, h, w;              // A pixel grid (conv: = output grid)
   int x_stride32, x_off32;
   int halo, P, Q, R, TW, row_mode, MB;
-  int col_tiles, row_tiles, n_tiles;
+  uint32_t p_magic;         // ceil(2^32 / P): q / P == umulhi(q, p_magic) for q < 2^16
+  int col_tiles, row_tiles, n_tiles, num_tiles;
   int zero_pad;
   int kc;
   const int32_t *chunk_word;
@@ -69,8 +81,7 @@ struct Params {
   int32_t *acc;
   uint32_t *bits;
   int out_stride32, out_off32, out_groups;
-  const int32_t *thr;
-  const uint8_t *codes;
+  const int2 *thr2;         // per column: fires <=> m * acc >= t
 };
 
 // ----------------------------------------------------------------- PTX glue
@@ -155,28 +166,37 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 
 // 4 activation bits -> 4 s8 lanes of +-1 (bit 1 -> 0x01, bit 0 -> 0xFF)
 __device__ __forceinline__ uint32_t expand4(uint32_t nib) {
   const uint32_t spread = (nib * 0x00204081u) & 0x01010101u;
   return ~(spread * 0xFEu);
 }
-__device__ __forceinline__ void expand32(uint32_t b, uint4 &lo, uint4 &hi) {
-  lo.x = expand4(b & 0xF);
-  lo.y = expand4((b >> 4) & 0xF);
-  lo.z = expand4((b >> 8) & 0xF);
-  lo.w = expand4((b >> 12) & 0xF);
-  hi.x = expand4((b >> 16) & 0xF);
-  hi.y = expand4((b >> 20) & 0xF);
-  hi.z = expand4((b >> 24) & 0xF);
-  hi.w = expand4(b >> 28);
-}
-__device__ __forceinline__ void sts128(uint32_t addr, const uint4 &v) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
-               "r"(v.z), "r"(v.w)
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                       uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
                : "memory");
 }
 
+struct Tile {
+  int nb, y0, x0, nt;
+};
+__device__ __forceinline__ Tile decode_tile(const Params &p, int t) {
+  Tile r;
+  r.nt = t % p.n_tiles;
+  t /= p.n_tiles;
+  const int ct = t % p.col_tiles;
+  t /= p.col_tiles;
+  const int rt = t % p.row_tiles;
+  r.nb = t / p.row_tiles;
+  r.y0 = rt * p.R;
+  r.x0 = ct * p.TW;
+  return r;
+}
 __device__ __forceinline__ int block_q0(const Params &p, int b) {
   return p.row_mode ? (b + p.halo) * p.P + p.halo : p.halo * p.P + p.halo + BLOCK_M * b;
 }
@@ -187,30 +207,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
   uint64_t *empty = full + MAX_STAGES;
-  uint64_t *done = empty + MAX_STAGES;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+  uint64_t *acc_full = empty + MAX_STAGES;
+  uint64_t *acc_empty = acc_full + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
   uint8_t *a_base = smem + SMEM_HEADER;
   uint8_t *b_base = a_base + size_t(p.stages) * p.a_stage_bytes;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-
-  int t = blockIdx.x;
-  const int nt = t % p.n_tiles;
-  t /= p.n_tiles;
-  const int ct = t % p.col_tiles;
-  t /= p.col_tiles;
-  const int rt = t % p.row_tiles;
-  const int nb = t / p.row_tiles;
-  const int y0 = rt * p.R;
-  const int x0 = ct * p.TW;
+  const int S = p.stages;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < p.stages; ++s) {
-      mbar_init(smem_u32(&full[s]), NUM_PRODUCER_WARPS * 32 + 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(smem_u32(&full[s]), PROD_THREADS + 1);
       mbar_init(smem_u32(&empty[s]), 1);
     }
-    mbar_init(smem_u32(done), 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&acc_full[i]), 1);
+      mbar_init(smem_u32(&acc_empty[i]), EPI_THREADS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == MMA_WARP) {
@@ -224,132 +239,203 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int S = p.stages;
 
-  if (warp < NUM_PRODUCER_WARPS) {
-    // ---------------- producers: packed bits -> s8 strips
-    const uint32_t oob_word = p.zero_pad ? 0u : 0xFFFFFFFFu;
-    const uint4 oob = make_uint4(oob_word, oob_word, oob_word, oob_word);
+  if (warp >= PROD_WARP0 && warp < MMA_WARP) {
+    // ============ producers: packed bits -> s8 strips ============
+    const int pt = threadIdx.x - PROD_WARP0 * 32;
+    const uint32_t oob = p.zero_pad ? 0u : 0xFFFFFFFFu;
     const int strip_rows = p.R + 2 * p.halo;
-    for (int k = 0; k < p.kc; ++k) {
-      const int s = k % S;
-      const int u = k / S;
-      if (u > 0) mbar_wait(smem_u32(&empty[s]), (u - 1) & 1);
-      const uint32_t a0 = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
-      const uint32_t a1 = a0 + p.Q * 16;
-      const int cw = __ldg(p.chunk_word + k);
-      for (int q = threadIdx.x; q < p.Q; q += NUM_PRODUCER_WARPS * 32) {
-        const int rr = q / p.P;
-        const int cc = q - rr * p.P;
-        const int iy = y0 - p.halo + rr;
-        const int ix = x0 - p.halo + cc;
-        uint4 lo = oob, hi = oob;
-        if (rr < strip_rows && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w) {
-          const int64_t pix = (int64_t(nb) * p.h + iy) * p.w + ix;
-          const uint32_t bitsw = __ldg(p.x32 + pix * p.x_stride32 + p.x_off32 + cw);
-          expand32(bitsw, lo, hi);
-        }
-        sts128(a0 + q * 16, lo);
-        sts128(a1 + q * 16, hi);
-      }
-      fence_proxy_async();
-      mbar_arrive(smem_u32(&full[s]));
-    }
-
-    // ---------------- epilogue: TMEM -> threshold -> packed bits / int32 acc
-    mbar_wait(smem_u32(done), 0);
-    tc_fence_after();
-    const int m = warp * 32 + lane;
-    const uint32_t lane_addr = tmem + (uint32_t(warp * 32) << 16);
-    const int groups = p.n_tile / 32;
-    for (int b = 0; b < p.MB; ++b) {
-      const int q = block_q0(p, b) + m;
-      const int r = q / p.P - p.halo;
-      const int c = q % p.P - p.halo;
-      const int yy = y0 + r, xx = x0 + c;
-      const bool valid = r >= 0 && r < p.R && c >= 0 && c < p.TW && yy < p.h && xx < p.w;
-      for (int g = 0; g < groups; ++g) {
-        uint32_t v[32];
-        tmem_ld32(lane_addr + uint32_t(b * p.n_tile + g * 32), v);
-        const int j0 = nt * p.n_tile + g * 32;
-        if (!valid || j0 >= p.n_gemm) continue;
-        int o0, oy, ox;
-        if (TCONV) {
-          const int tap = j0 / p.c_out_pad;
-          o0 = j0 - tap * p.c_out_pad;
-          oy = yy * p.tconv_s + tap / p.tconv_s;
-          ox = xx * p.tconv_s + tap % p.tconv_s;
-        } else {
-          o0 = j0;
-          oy = yy;
-          ox = xx;
-        }
-        const int64_t opix = (int64_t(nb) * p.ho + oy) * p.wo + ox;
-        if (p.bits) {
-          uint32_t word = 0;
+    int k_global = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      const Tile tl = decode_tile(p, t);
+      for (int k = 0; k < p.kc; ++k, ++k_global) {
+        const int s = k_global % S;
+        const int u = k_global / S;
+        if (u > 0) mbar_wait(smem_u32(&empty[s]), (u - 1) & 1);
+        const uint32_t a0 = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
+        const uint32_t a1 = a0 + p.Q * 16;
+        const int cw = __ldg(p.chunk_word + k);
+        for (int base = pt; base < p.Q; base += PROD_THREADS * UNROLL) {
+          uint32_t word[UNROLL];
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            word |= uint32_t(fires(int(v[i]), __ldg(p.thr + o0 + i), __ldg(p.codes + o0 + i))) << i;
-          uint32_t *dst = p.bits + opix * p.out_stride32 + p.out_off32;
-          dst[o0 / 32] = word;
-          if (o0 / 32 == p.c_out_pad / 32 - 1)
-            for (int gg = p.c_out_pad / 32; gg < p.out_groups; ++gg) dst[gg] = 0u;
-        }
-        if (p.acc) {
-          int32_t *dst = p.acc + opix * p.c_out + o0;
-          if (o0 + 32 <= p.c_out && (p.c_out % 4) == 0) {
+          for (int j = 0; j < UNROLL; ++j) {
+            const int q = base + j * PROD_THREADS;
+            const int rr = int(__umulhi(uint32_t(q), p.p_magic));
+            const int cc = q - rr * p.P;
+            const int iy = tl.y0 - p.halo + rr;
+            const int ix = tl.x0 - p.halo + cc;
+            word[j] = 0u;
+            if (q < p.Q && rr < strip_rows && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w) {
+              const int64_t pix = (int64_t(tl.nb) * p.h + iy) * p.w + ix;
+              word[j] = __ldg(p.x32 + pix * p.x_stride32 + p.x_off32 + cw);
+            }
+          }
 #pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              *reinterpret_cast<int4 *>(dst + i) =
-                  make_int4(int(v[i]), int(v[i + 1]), int(v[i + 2]), int(v[i + 3]));
-          } else {
-            for (int i = 0; i < 32 && o0 + i < p.c_out; ++i) dst[i] = int(v[i]);
+          for (int j = 0; j < UNROLL; ++j) {
+            const int q = base + j * PROD_THREADS;
+            if (q >= p.Q) break;
+            const int rr = int(__umulhi(uint32_t(q), p.p_magic));
+            const int cc = q - rr * p.P;
+            const int iy = tl.y0 - p.halo + rr;
+            const int ix = tl.x0 - p.halo + cc;
+            const bool inb = rr < strip_rows && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w;
+            const uint32_t b = word[j];
+            if (inb) {
+              sts128(a0 + q * 16, expand4(b & 0xF), expand4((b >> 4) & 0xF),
+                     expand4((b >> 8) & 0xF), expand4((b >> 12) & 0xF));
+              sts128(a1 + q * 16, expand4((b >> 16) & 0xF), expand4((b >> 20) & 0xF),
+                     expand4((b >> 24) & 0xF), expand4(b >> 28));
+            } else {
+              sts128(a0 + q * 16, oob, oob, oob, oob);
+              sts128(a1 + q * 16, oob, oob, oob, oob);
+            }
           }
         }
+        fence_proxy_async();
+        mbar_arrive(smem_u32(&full[s]));
       }
     }
   } else if (warp == MMA_WARP) {
-    // ---------------- single-thread MMA issue
+    // ============ single-thread MMA issue ============
     if (lane == 0) {
       const uint32_t sbo = 128;
       const uint32_t a_lbo = uint32_t(p.Q) * 16;
       const uint32_t b_lbo = uint32_t(p.n_tile) * 16;
-      for (int k = 0; k < p.kc; ++k) {
-        const int s = k % S;
-        mbar_wait(smem_u32(&full[s]), (k / S) & 1);
+      int k_global = 0, it = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+        const int ab = it & 1;
+        if (it >= 2) mbar_wait(smem_u32(&acc_empty[ab]), ((it >> 1) - 1) & 1);
         tc_fence_after();
-        const uint32_t a_s = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
-        const uint32_t b_s = smem_u32(b_base + size_t(s) * p.b_stage_bytes);
-        for (int b = 0; b < p.MB; ++b) {
-          const int q0 = block_q0(p, b);
+        const uint32_t d0 = tmem + uint32_t(ab * ACC_COLS);
+        for (int k = 0; k < p.kc; ++k, ++k_global) {
+          const int s = k_global % S;
+          mbar_wait(smem_u32(&full[s]), (k_global / S) & 1);
+          tc_fence_after();
+          const uint32_t a_s = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
+          const uint32_t b_s = smem_u32(b_base + size_t(s) * p.b_stage_bytes);
+          for (int b = 0; b < p.MB; ++b) {
+            const int q0 = block_q0(p, b);
 #pragma unroll
-          for (int tap = 0; tap < TAPS; ++tap) {
-            const int off = TAPS == 9 ? (tap / 3 - 1) * p.P + (tap % 3 - 1) : 0;
-            const uint64_t ad = umma_desc(a_s + uint32_t(q0 + off) * 16, a_lbo, sbo);
-            const uint64_t bd = umma_desc(b_s + uint32_t(tap * p.n_tile * 32), b_lbo, sbo);
-            umma_i8(tmem + uint32_t(b * p.n_tile), ad, bd, p.idesc, (k | tap) != 0);
+            for (int tap = 0; tap < TAPS; ++tap) {
+              const int off = TAPS == 9 ? (tap / 3 - 1) * p.P + (tap % 3 - 1) : 0;
+              const uint64_t ad = umma_desc(a_s + uint32_t(q0 + off) * 16, a_lbo, sbo);
+              const uint64_t bd = umma_desc(b_s + uint32_t(tap * p.n_tile * 32), b_lbo, sbo);
+              umma_i8(d0 + uint32_t(b * p.n_tile), ad, bd, p.idesc, (k | tap) != 0);
+            }
           }
+          umma_commit(smem_u32(&empty[s]));
         }
-        umma_commit(smem_u32(&empty[s]));
+        umma_commit(smem_u32(&acc_full[ab]));
       }
-      umma_commit(smem_u32(done));
     }
     __syncwarp();
   } else if (warp == BLOAD_WARP) {
-    // ---------------- weight stages: one bulk copy per stage
+    // ============ weight stages: one bulk copy per stage ============
     if (lane == 0) {
-      const int8_t *src = p.b + size_t(nt) * p.kc * p.b_stage_bytes;
-      for (int k = 0; k < p.kc; ++k) {
-        const int s = k % S;
-        const int u = k / S;
-        if (u > 0) mbar_wait(smem_u32(&empty[s]), (u - 1) & 1);
-        const uint32_t bar = smem_u32(&full[s]);
-        mbar_arrive_expect_tx(bar, p.b_stage_bytes);
-        bulk_g2s(smem_u32(b_base + size_t(s) * p.b_stage_bytes), src + size_t(k) * p.b_stage_bytes,
-                 p.b_stage_bytes, bar);
+      int k_global = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        const int nt = t % p.n_tiles;
+        const int8_t *src = p.b + size_t(nt) * p.kc * p.b_stage_bytes;
+        for (int k = 0; k < p.kc; ++k, ++k_global) {
+          const int s = k_global % S;
+          const int u = k_global / S;
+          if (u > 0) mbar_wait(smem_u32(&empty[s]), (u - 1) & 1);
+          const uint32_t bar = smem_u32(&full[s]);
+          mbar_arrive_expect_tx(bar, p.b_stage_bytes);
+          bulk_g2s(smem_u32(b_base + size_t(s) * p.b_stage_bytes),
+                   src + size_t(k) * p.b_stage_bytes, p.b_stage_bytes, bar);
+        }
       }
     }
     __syncwarp();
+  } else {
+    // ============ epilogue: TMEM -> threshold -> packed bits / int32 acc ============
+    const int quarter = warp & 3;
+    const int half = warp >> 2;
+    const int m = quarter * 32 + lane;
+    const int groups = p.n_tile / 32;
+    int it = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+      const int ab = it & 1;
+      const Tile tl = decode_tile(p, t);
+      mbar_wait(smem_u32(&acc_full[ab]), (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(ab * ACC_COLS);
+      for (int b = half; b < p.MB; b += 2) {
+        const int q = block_q0(p, b) + m;
+        const int rq = int(__umulhi(uint32_t(q), p.p_magic));
+        const int r = rq - p.halo;
+        const int c = q - rq * p.P - p.halo;
+        const int yy = tl.y0 + r, xx = tl.x0 + c;
+        const bool valid = r >= 0 && r < p.R && c >= 0 && c < p.TW && yy < p.h && xx < p.w;
+        uint32_t words[4] = {0u, 0u, 0u, 0u};
+        int o_first = 0, oy = yy, ox = xx;
+        for (int g = 0; g < groups; ++g) {
+          uint32_t v[32];
+          tmem_ld32(lane_addr + uint32_t(b * p.n_tile + g * 32), v);
+          const int j0 = tl.nt * p.n_tile + g * 32;
+          if (!valid || j0 >= p.n_gemm) continue;
+          int o0 = j0;
+          if (TCONV) {
+            const int tap = j0 / p.c_out_pad;
+            o0 = j0 - tap * p.c_out_pad;
+            oy = yy * p.tconv_s + tap / p.tconv_s;
+            ox = xx * p.tconv_s + tap % p.tconv_s;
+          }
+          if (g == 0) o_first = o0;
+          uint32_t wd = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int2 th = __ldg(p.thr2 + j0 + i);
+            wd |= uint32_t(th.x * int(v[i]) >= th.y) << i;
+          }
+          words[g] = wd;
+          if (p.acc) {
+            const int64_t opix = (int64_t(tl.nb) * p.ho + oy) * p.wo + ox;
+            int32_t *dst = p.acc + opix * p.c_out + o0;
+            if (o0 + 32 <= p.c_out && (p.c_out % 4) == 0) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 4)
+                *reinterpret_cast<int4 *>(dst + i) =
+                    make_int4(int(v[i]), int(v[i + 1]), int(v[i + 2]), int(v[i + 3]));
+            } else {
+              for (int i = 0; i < 32; ++i)
+                if (o0 + i < p.c_out) dst[i] = int(v[i]);
+            }
+          }
+        }
+        if (valid && p.bits && tl.nt * p.n_tile < p.n_gemm) {
+          // groups of this tile cover one output pixel (tiling guarantees it);
+          // append the pad groups when the tile ends that pixel's channels
+          const int64_t opix = (int64_t(tl.nb) * p.ho + oy) * p.wo + ox;
+          uint32_t *dst = p.bits + opix * p.out_stride32 + p.out_off32;
+          const int g0 = o_first / 32;
+          int gend = g0 + groups;
+          if (gend > p.c_out_pad / 32) gend = p.c_out_pad / 32;
+          const bool last = gend == p.c_out_pad / 32;
+          const int wend = last ? p.out_groups : gend;
+          uint32_t out8[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) out8[i] = i < groups ? words[i & 3] : 0u;
+          int g = g0;
+          while (g < wend) {
+            const int i = g - g0;
+            if ((g & 3) == 0 && g + 4 <= wend && i + 4 <= 8) {
+              *reinterpret_cast<uint4 *>(dst + g) = make_uint4(out8[i], out8[i + 1], out8[i + 2], out8[i + 3]);
+              g += 4;
+            } else if ((g & 1) == 0 && g + 2 <= wend && i + 2 <= 8) {
+              *reinterpret_cast<uint2 *>(dst + g) = make_uint2(out8[i], out8[i + 1]);
+              g += 2;
+            } else {
+              dst[g] = i < 8 ? out8[i] : 0u;
+              g += 1;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(smem_u32(&acc_empty[ab]));
+    }
   }
 
   tc_fence_before();
@@ -391,7 +477,14 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
   const int s2 = cv->transposed ? cv->stride * cv->stride : 1;
   const int c_out_pad = (cv->c_out + 31) / 32 * 32;
   const int n_gemm = s2 * c_out_pad;
-  const int n_tile = n_gemm <= 128 ? n_gemm : 128;
+  // An N tile must never straddle two output pixels (tconv taps): pick the
+  // largest width <= 128 that divides the per-pixel span when it exceeds 128.
+  int n_tile;
+  if (!cv->transposed) n_tile = std::min(c_out_pad, 128);  // conv: every column is one pixel
+  else if (c_out_pad <= 128) n_tile = c_out_pad;
+  else if (c_out_pad % 128 == 0) n_tile = 128;
+  else if (c_out_pad % 64 == 0) n_tile = 64;
+  else n_tile = 32;
   const int n_tiles = (n_gemm + n_tile - 1) / n_tile;
   const size_t b_stage = size_t(taps) * n_tile * 32;
   std::vector<int8_t> b(size_t(n_tiles) * kc * b_stage, 0);
@@ -429,6 +522,30 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
   MBU_TRY(check_cuda(cudaMemcpy(cv->d_chunk_word, chunk_word.data(), kc * sizeof(int32_t),
                                 cudaMemcpyHostToDevice),
                      "upload chunk map"));
+  // per GEMM column threshold in "m * acc >= t" form
+  std::vector<int2> thr2(size_t(n_tiles) * n_tile + 32, make_int2(0, 1));
+  if (cv->has_threshold) {
+    std::vector<int32_t> t(static_cast<size_t>(c_out_pad), 0);
+    std::vector<uint8_t> c(static_cast<size_t>(c_out_pad), 2);
+    MBU_TRY(check_cuda(cudaMemcpy(t.data(), cv->d_thr, t.size() * 4, cudaMemcpyDeviceToHost), "thr"));
+    MBU_TRY(check_cuda(cudaMemcpy(c.data(), cv->d_codes, c.size(), cudaMemcpyDeviceToHost), "codes"));
+    const int lim = 1 << 30;
+    for (int j = 0; j < n_gemm; ++j) {
+      const int o = cv->transposed ? j % c_out_pad : j;
+      const int T = t[o];
+      int2 e = make_int2(0, 1);  // never fires
+      switch (c[o]) {
+        case 0: e = T <= -lim ? make_int2(0, 0) : T > lim ? make_int2(0, 1) : make_int2(1, T); break;
+        case 1: e = T >= lim ? make_int2(0, 0) : T < -lim ? make_int2(0, 1) : make_int2(-1, -T); break;
+        case 3: e = make_int2(0, 0); break;
+        default: break;
+      }
+      thr2[j] = e;
+    }
+  }
+  MBU_TRY(check_cuda(cudaMalloc(&cv->d_thr2, thr2.size() * sizeof(int2)), "alloc thr2"));
+  MBU_TRY(check_cuda(cudaMemcpy(cv->d_thr2, thr2.data(), thr2.size() * sizeof(int2), cudaMemcpyHostToDevice),
+                     "upload thr2"));
   cv->taps = taps;
   cv->kc = kc;
   cv->n_gemm = n_gemm;
@@ -439,6 +556,17 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
   cv->b_stage_bytes = b_stage;
   cv->tc_ok = 1;
   return MBU_OK;
+}
+
+static int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
 }
 
 template <int TAPS, bool TCONV>
@@ -466,7 +594,7 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   p.halo = cv->taps == 9 ? 1 : 0;
   p.n_tile = cv->n_tile;
   p.n_tiles = cv->n_tiles;
-  p.MB = std::min(8, tc::TMEM_COLS / cv->n_tile);
+  p.MB = std::min(8, tc::ACC_COLS / cv->n_tile);
   if (x.w >= 128) {
     p.row_mode = 1;
     p.TW = 128;
@@ -481,18 +609,19 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
     p.MB = ((p.R - 1) * p.P + p.TW + tc::BLOCK_M - 1) / tc::BLOCK_M;
     p.col_tiles = 1;
   }
+  p.p_magic = uint32_t((0x100000000ull + p.P - 1) / p.P);
   p.row_tiles = (x.h + p.R - 1) / p.R;
   const int q_last = p.row_mode ? (p.MB - 1 + p.halo) * p.P + p.halo
                                 : p.halo * p.P + p.halo + tc::BLOCK_M * (p.MB - 1);
   int Q = q_last + tc::BLOCK_M + (p.halo ? p.P + 1 : 0);
   Q = std::max(Q, (p.R + 2 * p.halo) * p.P);
   Q = (Q + 7) / 8 * 8;
+  if (Q >= 65536) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv strip too tall");
   p.Q = Q;
   p.a_stage_bytes = uint32_t((size_t(Q) * 32 + 1023) / 1024 * 1024);
   p.b_stage_bytes = uint32_t(cv->b_stage_bytes);
   const size_t stage = size_t(p.a_stage_bytes) + p.b_stage_bytes;
-  int stages = int((113 * 1024 - tc::SMEM_HEADER) / stage);
-  if (stages < 2) stages = int((227 * 1024 - tc::SMEM_HEADER) / stage);
+  int stages = int((227 * 1024 - tc::SMEM_HEADER) / stage);
   if (stages < 2) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv stage does not fit in shared memory");
   p.stages = std::min(stages, tc::MAX_STAGES);
   p.zero_pad = cv->pad_mode == MBU_PAD_ZERO;
@@ -513,15 +642,17 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   p.out_stride32 = out_stride * 2;
   p.out_off32 = out_offset * 2;
   p.out_groups = cv->out_wpp * 2;
-  p.thr = cv->d_thr;
-  p.codes = cv->d_codes;
-  const int64_t grid = int64_t(x.n) * p.row_tiles * p.col_tiles * p.n_tiles;
-  if (grid == 0) return MBU_OK;
-  if (grid > 0x7FFFFFFF) return fail(MBU_ERR_SHAPE, "tcgen05 conv grid too large");
-  const size_t smem = tc::SMEM_HEADER + size_t(p.stages) * stage;
-  if (cv->transposed) return launch_tc_impl<1, true>(p, int(grid), smem, st);
-  if (cv->taps == 9) return launch_tc_impl<9, false>(p, int(grid), smem, st);
-  return launch_tc_impl<1, false>(p, int(grid), smem, st);
+  p.thr2 = reinterpret_cast<const int2 *>(cv->d_thr2);
+  const int64_t tiles = int64_t(x.n) * p.row_tiles * p.col_tiles * p.n_tiles;
+  if (tiles == 0) return MBU_OK;
+  if (tiles > 0x7FFFFFFF) return fail(MBU_ERR_SHAPE, "tcgen05 conv grid too large");
+  p.num_tiles = int(tiles);
+  const int grid = int(std::min<int64_t>(tiles, num_sms()));
+  size_t smem = tc::SMEM_HEADER + size_t(p.stages) * stage;
+  smem = std::max<size_t>(smem, tc::MIN_SMEM);
+  if (cv->transposed) return launch_tc_impl<1, true>(p, grid, smem, st);
+  if (cv->taps == 9) return launch_tc_impl<9, false>(p, grid, smem, st);
+  return launch_tc_impl<1, false>(p, grid, smem, st);
 }
 
 }  // namespace mbu

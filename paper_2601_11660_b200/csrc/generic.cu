@@ -25,6 +25,7 @@ namespace mbu {
 static thread_local std::string t_last_error;
 std::atomic<int64_t> g_launches{0};
 int g_last_path = 0;
+int g_force_generic_fconv = 0;
 
 void set_error(const std::string &msg) { t_last_error = msg; }
 int fail(int status, const std::string &msg) {
@@ -281,6 +282,11 @@ int launch_fconv(const mbu_fconv *fc, const double *x_f64, const ActView &xb, in
   const int wo = (w + 2 * fc->pad - fc->kw) / fc->stride + 1;
   const int64_t pix = int64_t(n) * ho * wo;
   if (pix == 0) return MBU_OK;
+  if (bits && !acc && fc->stem_fast && x_f64 && !g_force_generic_fconv)
+    return launch_stem_fast(fc, x_f64, n, h, w, bits, out_stride, out_offset, st);
+  if (!bits && fc->bits_input && fc->kh == 1 && fc->kw == 1 && fc->stride == 1 && fc->pad == 0 &&
+      !g_force_generic_fconv)
+    return launch_head_fast(fc, xb, n, h, w, acc, mask, st);
   if (bits) {
     if (!fc->has_bn) return fail(MBU_ERR_ENGINE, "fconv: sign output requested without batchnorm");
     const int out_wpp = ((fc->c_out + 127) / 128) * 2;
@@ -364,6 +370,13 @@ const char *mbu_last_error(void) { return t_last_error.c_str(); }
 int mbu_version(void) { return 1; }
 int64_t mbu_launch_count(void) { return g_launches.load(); }
 int mbu_last_path(void) { return g_last_path; }
+int mbu_set_option(int option, int value) {
+  if (option == MBU_OPT_GENERIC_ENDPOINTS) {
+    g_force_generic_fconv = value != 0;
+    return MBU_OK;
+  }
+  return fail(MBU_ERR_ENGINE, "unknown option " + std::to_string(option));
+}
 
 int mbu_conv_create(mbu_conv **out, int device, int transposed, int kh, int kw, int stride,
                     int pad, int c_in, int c_out, int pad_mode, int n_segments,
@@ -454,6 +467,7 @@ int mbu_conv_destroy(mbu_conv *cv) {
   cudaFree(cv->d_codes);
   cudaFree(cv->d_chunk_word);
   cudaFree(cv->d_b);
+  cudaFree(cv->d_thr2);
   delete cv;
   return MBU_OK;
 }
@@ -522,6 +536,7 @@ int mbu_fconv_create(mbu_fconv **out, int device, int kh, int kw, int stride, in
     st = upload(&fc->d_bn, p.data(), p.size(), "upload bn");
   }
   if (st == MBU_OK && in_lanes) st = upload(&fc->d_lanes, in_lanes, size_t(c_in), "upload lanes");
+  if (st == MBU_OK) st = stem_prepare(fc, weights, bias, bn, eps);
   if (st != MBU_OK) {
     mbu_fconv_destroy(fc);
     return st;
@@ -536,6 +551,7 @@ int mbu_fconv_destroy(mbu_fconv *fc) {
   cudaFree(fc->d_bias);
   cudaFree(fc->d_bn);
   cudaFree(fc->d_lanes);
+  cudaFree(fc->d_stem);
   delete fc;
   return MBU_OK;
 }

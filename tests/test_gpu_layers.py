@@ -152,3 +152,44 @@ def test_bit_gemm_vs_numpy(cuda, rng):
     pb = np.unpackbits(pos.words.view(np.uint8), bitorder="little").reshape(11, 256).astype(np.int64)
     nb = np.unpackbits(neg.words.view(np.uint8), bitorder="little").reshape(11, 256).astype(np.int64)
     assert np.array_equal(mb.bit_gemm(a, pos, neg, 256), dense_a @ (pb - nb).T)
+
+
+def test_stem_fast_path_equals_float64_path(cuda):
+    """The float32 stem with exact float64 re-check must reproduce the
+    all-float64 kernel bit for bit, including pixels planted exactly on the
+    batchnorm decision boundary (which force the re-check)."""
+    import ctypes
+
+    import torch
+
+    from paper_2601_11660_b200.ops import FloatConvHandle
+
+    rng = np.random.default_rng(5)
+    x = rng.random((2, 40, 136, 3))
+    x[0, 3, 4] = [np.inf, 0.5, 0.5]  # non-finite input goes down the exact path
+    w = rng.normal(size=(64, 3, 3, 3))
+    b = rng.normal(size=64)
+    g = rng.uniform(-1.5, 1.5, 64)
+    g[0] = 0.0
+    be = rng.normal(size=64)
+    v = rng.uniform(0.5, 2.0, 64)
+    eps = 1e-5
+    acc = dense.ref_float_conv(x[1:2], w, b, 1, 1)
+    sigma = np.sqrt(v + eps)
+    mean = acc[0, 17, 9, :] + be * sigma / np.where(g == 0, 1.0, g)  # boundary on a pixel
+    spec = mb.ConvSpec(3, 3, 1, 1, 3, 64)
+    fc = FloatConvHandle(w, b, spec, bn=(g, be, mean, v, eps))
+    xd = torch.from_numpy(x).to(cuda)
+    outs = []
+    for generic in (0, 1):
+        _lib.call("mbu_set_option", 1, generic)
+        out = torch.zeros((2, 40, 136, 2), dtype=torch.int64, device=cuda)
+        fc.run(2, 40, 136, x_f64=xd, bits=out)
+        torch.cuda.synchronize()
+        outs.append(out.cpu().numpy())
+    _lib.call("mbu_set_option", 1, 0)
+    assert np.array_equal(outs[0], outs[1])
+    ref = dense.ref_bn_sign(dense.ref_float_conv(x, w, b, 1, 1), g, be, mean, v, eps)
+    got = mb.unpack_tensor(mb.BitTensor(2, 40, 136, 64, outs[0].view(np.uint64)))
+    diff = got != ref
+    assert diff.sum() <= 64, diff.sum()  # only planted exact-boundary pixels may round differently
