@@ -287,26 +287,32 @@ def run_ours(args):
     # ---- end to end through the public engine: pinned H2D + forward + D2H
     e2e = None
     if not args.no_e2e:
-        host_img = torch.empty(eng.shape, dtype=torch.float64, pin_memory=True)
-        host_img.copy_(eng.image.cpu())
-        host_logits = torch.empty(eng.out_shape, dtype=torch.float64, pin_memory=True)
-        host_mask = torch.empty(eng.out_shape, dtype=torch.uint8, pin_memory=True)
-        for _ in range(args.warmup):
-            eng.run_e2e(host_img, host_logits, host_mask)
+        # two distinct pinned host frames batches, two result buffers
+        host_imgs = []
+        for i in range(2):
+            hb = torch.empty(eng.shape, dtype=torch.float64, pin_memory=True)
+            hb.copy_(torch.rand(eng.shape, dtype=torch.float64, device=dev, generator=g).cpu())
+            host_imgs.append(hb)
+        host_logits = [torch.empty(eng.out_shape, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+        host_masks = [torch.empty(eng.out_shape, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        eng.run_stream(host_imgs, host_logits, host_masks, args.warmup)
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
-        e0.record(st)
-        for _ in range(args.steps):
-            eng.run_e2e(host_img, host_logits, host_mask)
-        e1.record(st)
+        e0.record(eng.h2d)
+        eng.run_stream(host_imgs, host_logits, host_masks, args.steps)
+        e1.record(eng.d2h)
         torch.cuda.synchronize()
         barrier()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1))
         e2e = {"value": world * BATCH * args.steps / (e2e_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": host_img.numel() * 8,
-               "d2h_bytes_per_step": host_logits.numel() * 8 + host_mask.numel(),
-               "ms_per_step": e2e_ms / args.steps}
+               "h2d_bytes_per_step": host_imgs[0].numel() * 8,
+               "d2h_bytes_per_step": host_logits[0].numel() * 8 + host_masks[0].numel(),
+               "ms_per_step": e2e_ms / args.steps,
+               "how": "Engine.run_stream: pinned float64 images H2D on a copy stream, CUDA-graph "
+                      "forward, float64 logits + uint8 mask D2H on a second copy stream; two "
+                      "device buffer sets overlap step i's compute with i+1's upload / i-1's "
+                      "download"}
     clk = clocks.stop()
 
     line = None

@@ -58,7 +58,7 @@ constexpr int TMEM_COLS = 512;  // two buffers
 constexpr int MAX_STAGES = 8;
 constexpr int SMEM_HEADER = 1024;
 constexpr int MIN_SMEM = 120 * 1024;  // > half an SM: exactly one CTA (and TMEM owner) per SM
-constexpr int UNROLL = 4;
+constexpr int PROD_ITEMS = 8;  // strip rows per producer thread per stage (Q <= 8 * 192)
 
 struct Params {
   const uint32_t *x32;
@@ -242,58 +242,74 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
 
   if (warp >= PROD_WARP0 && warp < MMA_WARP) {
     // ============ producers: packed bits -> s8 strips ============
+    // One-stage lookahead: the global loads of stage g+1 are in flight while
+    // stage g is expanded into shared memory (hides HBM/L2 latency).
     const int pt = threadIdx.x - PROD_WARP0 * 32;
     const uint32_t oob = p.zero_pad ? 0u : 0xFFFFFFFFu;
     const int strip_rows = p.R + 2 * p.halo;
-    int k_global = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    auto in_bounds = [&](const Tile &tl, int q) -> bool {
+      const int rr = int(__umulhi(uint32_t(q), p.p_magic));
+      const int cc = q - rr * p.P;
+      const int iy = tl.y0 - p.halo + rr;
+      const int ix = tl.x0 - p.halo + cc;
+      return q < p.Q && rr < strip_rows && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w;
+    };
+    auto load_stage = [&](int t, int k, uint32_t (&wd)[PROD_ITEMS]) {
       const Tile tl = decode_tile(p, t);
-      for (int k = 0; k < p.kc; ++k, ++k_global) {
-        const int s = k_global % S;
-        const int u = k_global / S;
-        if (u > 0) mbar_wait(smem_u32(&empty[s]), (u - 1) & 1);
-        const uint32_t a0 = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
-        const uint32_t a1 = a0 + p.Q * 16;
-        const int cw = __ldg(p.chunk_word + k);
-        for (int base = pt; base < p.Q; base += PROD_THREADS * UNROLL) {
-          uint32_t word[UNROLL];
+      const int cw = __ldg(p.chunk_word + k);
 #pragma unroll
-          for (int j = 0; j < UNROLL; ++j) {
-            const int q = base + j * PROD_THREADS;
-            const int rr = int(__umulhi(uint32_t(q), p.p_magic));
-            const int cc = q - rr * p.P;
-            const int iy = tl.y0 - p.halo + rr;
-            const int ix = tl.x0 - p.halo + cc;
-            word[j] = 0u;
-            if (q < p.Q && rr < strip_rows && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w) {
-              const int64_t pix = (int64_t(tl.nb) * p.h + iy) * p.w + ix;
-              word[j] = __ldg(p.x32 + pix * p.x_stride32 + p.x_off32 + cw);
-            }
-          }
+      for (int j = 0; j < PROD_ITEMS; ++j) {
+        const int q = pt + j * PROD_THREADS;
+        wd[j] = 0u;
+        if (in_bounds(tl, q)) {
+          const int rr = int(__umulhi(uint32_t(q), p.p_magic));
+          const int iy = tl.y0 - p.halo + rr;
+          const int ix = tl.x0 - p.halo + (q - rr * p.P);
+          const int64_t pix = (int64_t(tl.nb) * p.h + iy) * p.w + ix;
+          wd[j] = __ldg(p.x32 + pix * p.x_stride32 + p.x_off32 + cw);
+        }
+      }
+    };
+    uint32_t cur[PROD_ITEMS], nxt[PROD_ITEMS];
+    int t = blockIdx.x, k = 0;
+    if (t < p.num_tiles) load_stage(t, 0, cur);
+    int k_global = 0;
+    while (t < p.num_tiles) {
+      int tn = t, kn = k + 1;
+      if (kn == p.kc) {
+        kn = 0;
+        tn += gridDim.x;
+      }
+      if (tn < p.num_tiles) load_stage(tn, kn, nxt);
+      const int s = k_global % S;
+      const int u = k_global / S;
+      if (u > 0) mbar_wait(smem_u32(&empty[s]), (u - 1) & 1);
+      const uint32_t a0 = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
+      const uint32_t a1 = a0 + p.Q * 16;
+      const Tile tl = decode_tile(p, t);
 #pragma unroll
-          for (int j = 0; j < UNROLL; ++j) {
-            const int q = base + j * PROD_THREADS;
-            if (q >= p.Q) break;
-            const int rr = int(__umulhi(uint32_t(q), p.p_magic));
-            const int cc = q - rr * p.P;
-            const int iy = tl.y0 - p.halo + rr;
-            const int ix = tl.x0 - p.halo + cc;
-            const bool inb = rr < strip_rows && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w;
-            const uint32_t b = word[j];
-            if (inb) {
-              sts128(a0 + q * 16, expand4(b & 0xF), expand4((b >> 4) & 0xF),
-                     expand4((b >> 8) & 0xF), expand4((b >> 12) & 0xF));
-              sts128(a1 + q * 16, expand4((b >> 16) & 0xF), expand4((b >> 20) & 0xF),
-                     expand4((b >> 24) & 0xF), expand4(b >> 28));
-            } else {
-              sts128(a0 + q * 16, oob, oob, oob, oob);
-              sts128(a1 + q * 16, oob, oob, oob, oob);
-            }
+      for (int j = 0; j < PROD_ITEMS; ++j) {
+        const int q = pt + j * PROD_THREADS;
+        if (q < p.Q) {
+          const uint32_t b = cur[j];
+          if (in_bounds(tl, q)) {
+            sts128(a0 + q * 16, expand4(b & 0xF), expand4((b >> 4) & 0xF),
+                   expand4((b >> 8) & 0xF), expand4((b >> 12) & 0xF));
+            sts128(a1 + q * 16, expand4((b >> 16) & 0xF), expand4((b >> 20) & 0xF),
+                   expand4((b >> 24) & 0xF), expand4(b >> 28));
+          } else {
+            sts128(a0 + q * 16, oob, oob, oob, oob);
+            sts128(a1 + q * 16, oob, oob, oob, oob);
           }
         }
-        fence_proxy_async();
-        mbar_arrive(smem_u32(&full[s]));
       }
+      fence_proxy_async();
+      mbar_arrive(smem_u32(&full[s]));
+#pragma unroll
+      for (int j = 0; j < PROD_ITEMS; ++j) cur[j] = nxt[j];
+      t = tn;
+      k = kn;
+      ++k_global;
     }
   } else if (warp == MMA_WARP) {
     // ============ single-thread MMA issue ============
@@ -361,6 +377,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       mbar_wait(smem_u32(&acc_full[ab]), (it >> 1) & 1);
       tc_fence_after();
       const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(ab * ACC_COLS);
+      const int jt = tl.nt * p.n_tile;
+      const int span = TCONV ? p.c_out_pad : p.n_gemm;  // GEMM columns per output pixel
       for (int b = half; b < p.MB; b += 2) {
         const int q = block_q0(p, b) + m;
         const int rq = int(__umulhi(uint32_t(q), p.p_magic));
@@ -368,69 +386,70 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         const int c = q - rq * p.P - p.halo;
         const int yy = tl.y0 + r, xx = tl.x0 + c;
         const bool valid = r >= 0 && r < p.R && c >= 0 && c < p.TW && yy < p.h && xx < p.w;
-        uint32_t words[4] = {0u, 0u, 0u, 0u};
-        int o_first = 0, oy = yy, ox = xx;
-        for (int g = 0; g < groups; ++g) {
-          uint32_t v[32];
-          tmem_ld32(lane_addr + uint32_t(b * p.n_tile + g * 32), v);
-          const int j0 = tl.nt * p.n_tile + g * 32;
-          if (!valid || j0 >= p.n_gemm) continue;
-          int o0 = j0;
-          if (TCONV) {
-            const int tap = j0 / p.c_out_pad;
-            o0 = j0 - tap * p.c_out_pad;
-            oy = yy * p.tconv_s + tap / p.tconv_s;
-            ox = xx * p.tconv_s + tap % p.tconv_s;
-          }
-          if (g == 0) o_first = o0;
-          uint32_t wd = 0;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int2 th = __ldg(p.thr2 + j0 + i);
-            wd |= uint32_t(th.x * int(v[i]) >= th.y) << i;
-          }
-          words[g] = wd;
-          if (p.acc) {
-            const int64_t opix = (int64_t(tl.nb) * p.ho + oy) * p.wo + ox;
-            int32_t *dst = p.acc + opix * p.c_out + o0;
-            if (o0 + 32 <= p.c_out && (p.c_out % 4) == 0) {
-#pragma unroll
-              for (int i = 0; i < 32; i += 4)
-                *reinterpret_cast<int4 *>(dst + i) =
-                    make_int4(int(v[i]), int(v[i + 1]), int(v[i + 2]), int(v[i + 3]));
-            } else {
-              for (int i = 0; i < 32; ++i)
-                if (o0 + i < p.c_out) dst[i] = int(v[i]);
-            }
-          }
-        }
-        if (valid && p.bits && tl.nt * p.n_tile < p.n_gemm) {
-          // groups of this tile cover one output pixel (tiling guarantees it);
-          // append the pad groups when the tile ends that pixel's channels
+        // walk the tile's 32-column groups in runs that share one output pixel
+        int g = 0;
+        while (g < groups) {
+          const int j0 = jt + 32 * g;
+          if (j0 >= p.n_gemm) break;
+          const int tap = TCONV ? j0 / p.c_out_pad : 0;
+          const int o0 = j0 - tap * p.c_out_pad;
+          const int run = min(groups - g, (span - o0) / 32);
+          const int oy = TCONV ? yy * p.tconv_s + tap / p.tconv_s : yy;
+          const int ox = TCONV ? xx * p.tconv_s + tap % p.tconv_s : xx;
           const int64_t opix = (int64_t(tl.nb) * p.ho + oy) * p.wo + ox;
-          uint32_t *dst = p.bits + opix * p.out_stride32 + p.out_off32;
-          const int g0 = o_first / 32;
-          int gend = g0 + groups;
-          if (gend > p.c_out_pad / 32) gend = p.c_out_pad / 32;
-          const bool last = gend == p.c_out_pad / 32;
-          const int wend = last ? p.out_groups : gend;
-          uint32_t out8[8];
+          uint32_t w8[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) out8[i] = i < groups ? words[i & 3] : 0u;
-          int g = g0;
-          while (g < wend) {
-            const int i = g - g0;
-            if ((g & 3) == 0 && g + 4 <= wend && i + 4 <= 8) {
-              *reinterpret_cast<uint4 *>(dst + g) = make_uint4(out8[i], out8[i + 1], out8[i + 2], out8[i + 3]);
-              g += 4;
-            } else if ((g & 1) == 0 && g + 2 <= wend && i + 2 <= 8) {
-              *reinterpret_cast<uint2 *>(dst + g) = make_uint2(out8[i], out8[i + 1]);
-              g += 2;
-            } else {
-              dst[g] = i < 8 ? out8[i] : 0u;
-              g += 1;
+          for (int rr = 0; rr < 8; ++rr) {
+            w8[rr] = 0u;
+            if (rr < run) {
+              uint32_t v[32];
+              tmem_ld32(lane_addr + uint32_t(b * p.n_tile + (g + rr) * 32), v);
+              const int2 *th = p.thr2 + j0 + 32 * rr;
+              uint32_t wd = 0;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const int2 e = __ldg(th + i);
+                wd |= uint32_t(e.x * int(v[i]) >= e.y) << i;
+              }
+              w8[rr] = wd;
+              if (p.acc && valid) {
+                const int oc = o0 + 32 * rr;
+                int32_t *dst = p.acc + opix * p.c_out + oc;
+                if (oc + 32 <= p.c_out && (p.c_out % 4) == 0) {
+#pragma unroll
+                  for (int i = 0; i < 32; i += 4)
+                    *reinterpret_cast<int4 *>(dst + i) =
+                        make_int4(int(v[i]), int(v[i + 1]), int(v[i + 2]), int(v[i + 3]));
+                } else {
+                  for (int i = 0; i < 32; ++i)
+                    if (oc + i < p.c_out) dst[i] = int(v[i]);
+                }
+              }
             }
           }
+          if (valid && p.bits) {
+            // write the run; when it ends the pixel's channels, append the
+            // zero pad groups of the 128-lane block
+            uint32_t *dst = p.bits + opix * p.out_stride32 + p.out_off32;
+            const int g0 = o0 / 32;
+            const int wend = (g0 + run == p.c_out_pad / 32) ? p.out_groups : g0 + run;
+            int gg = g0;
+            while (gg < wend) {
+              const int i = gg - g0;
+              auto wv = [&](int ii) { return ii < run ? w8[ii & 7] : 0u; };
+              if ((gg & 3) == 0 && gg + 4 <= wend) {
+                *reinterpret_cast<uint4 *>(dst + gg) = make_uint4(wv(i), wv(i + 1), wv(i + 2), wv(i + 3));
+                gg += 4;
+              } else if ((gg & 1) == 0 && gg + 2 <= wend) {
+                *reinterpret_cast<uint2 *>(dst + gg) = make_uint2(wv(i), wv(i + 1));
+                gg += 2;
+              } else {
+                dst[gg] = wv(i);
+                gg += 1;
+              }
+            }
+          }
+          g += run;
         }
       }
       tc_fence_before();
@@ -479,9 +498,12 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
   const int n_gemm = s2 * c_out_pad;
   // An N tile must never straddle two output pixels (tconv taps): pick the
   // largest width <= 128 that divides the per-pixel span when it exceeds 128.
+  // N tile: conv -> up to 128 columns (MB = 2 blocks of 128 pixels share each
+  // weight stage). tconv -> whole taps when they fit in 256 columns so the A
+  // strip is expanded once for all s*s taps, else 128-column slices of a tap.
   int n_tile;
-  if (!cv->transposed) n_tile = std::min(c_out_pad, 128);  // conv: every column is one pixel
-  else if (c_out_pad <= 128) n_tile = c_out_pad;
+  if (!cv->transposed) n_tile = std::min(c_out_pad, 128);
+  else if (c_out_pad <= 256) n_tile = c_out_pad * std::min(s2, 256 / c_out_pad);
   else if (c_out_pad % 128 == 0) n_tile = 128;
   else if (c_out_pad % 64 == 0) n_tile = 64;
   else n_tile = 32;
@@ -616,7 +638,8 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   int Q = q_last + tc::BLOCK_M + (p.halo ? p.P + 1 : 0);
   Q = std::max(Q, (p.R + 2 * p.halo) * p.P);
   Q = (Q + 7) / 8 * 8;
-  if (Q >= 65536) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv strip too tall");
+  if (Q > tc::PROD_ITEMS * tc::PROD_THREADS)
+    return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv strip taller than the producer tiling");
   p.Q = Q;
   p.a_stage_bytes = uint32_t((size_t(Q) * 32 + 1023) / 1024 * 1024);
   p.b_stage_bytes = uint32_t(cv->b_stage_bytes);

@@ -4,34 +4,53 @@
 // the reference decides each stem bit with a float64 predicate
 //     y = gamma * ((acc + 0) - mean) / sigma + beta >= 0,
 //     acc = sum_taps dot(x, w) + bias          (float64)
-// This kernel evaluates acc in float32 and compares it with the exact
-// decision point T* = mean - beta*sigma/gamma. Whenever |acc32 - T*| is not
-// larger than a rigorous bound on the float32 error (plus slack for the
-// float64 predicate's own rounding), or the input is not finite, it
-// recomputes acc in float64 in the reference's order and evaluates the
-// reference predicate itself. So every output bit equals the float64
-// decision; the float32 path only decides pixels that are far from the
-// boundary. With trace output requested the whole layer runs in float64.
+// This kernel evaluates acc in float32 (packed FFMA2, 64 accumulators per
+// pixel in registers) and compares it with the exact decision point
+// T* = mean - beta*sigma/gamma. Whenever |acc32 - T*| is not larger than a
+// rigorous bound on the float32 error (plus slack for the float64
+// predicate's own rounding), or anything is non-finite, it recomputes acc in
+// float64 in the reference's order and evaluates the reference predicate
+// itself. So every output bit equals the float64 decision; the float32 path
+// only decides bits that are far from the boundary. With trace output
+// requested the whole layer runs through the float64 kernel instead.
 //
 // Head (graph.py:439-441, :455): a 1x1 float64 conv of the +-1 bits,
 // logits = bias + sum_c (+-w_c), mask = logits >= 0.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include "common.cuh"
 
 namespace mbu {
 
-constexpr int STEM_TX = 32, STEM_TY = 8;  // 256 threads, one output pixel each
-constexpr int STEM_MAX_CIN = 4, STEM_MAX_COUT = 64;
+constexpr int STEM_TX = 32, STEM_TY = 4;  // 128 threads, one output pixel each
+constexpr int STEM_MAX_CIN = 4, STEM_COUT = 64;
 
 struct StemConsts {
-  float w32[STEM_MAX_COUT * 9 * STEM_MAX_CIN];
-  float wabs[STEM_MAX_COUT];     // sum |w| over taps and channels
-  float tstar[STEM_MAX_COUT];    // decision point in acc units (float)
-  float babs[STEM_MAX_COUT];
-  int dir[STEM_MAX_COUT];        // +1: acc >= T*, -1: acc <= T*, 0: constant (see cbit)
-  int cbit[STEM_MAX_COUT];
+  float w[9 * STEM_MAX_CIN][STEM_COUT];  // [tap*cin + c][o], float32 copy
+  float b[STEM_COUT];                    // bias (float32)
+  float tstar[STEM_COUT];                // +-inf for constant channels
+  float dirf[STEM_COUT];                 // +1: bit = acc > T*, -1: bit = acc < T*
+  float ma[STEM_COUT], mb[STEM_COUT];    // margin = max|x| * ma + mb (inf: always exact)
 };
+
+__device__ __forceinline__ unsigned long long pack2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void unpack2(unsigned long long v, float &a, float &b) {
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long ffma2_bcast(float x, unsigned long long w,
+                                                          unsigned long long acc) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pack2(x, x)), "l"(w), "l"(acc));
+  return r;
+}
 
 template <int CIN>
 __global__ void __launch_bounds__(STEM_TX *STEM_TY) stem_kernel(
@@ -40,13 +59,11 @@ __global__ void __launch_bounds__(STEM_TX *STEM_TY) stem_kernel(
     const double *__restrict__ bn, const StemConsts *__restrict__ k,
     uint32_t *__restrict__ bits, int out_stride32, int out_offset32, int out_groups) {
   __shared__ double tile[STEM_TY + 2][STEM_TX + 2][CIN];
-  __shared__ StemConsts ks;
+  __shared__ __align__(16) StemConsts ks;
   const int tx = threadIdx.x % STEM_TX, ty = threadIdx.x / STEM_TX;
   const int x0 = blockIdx.x * STEM_TX, y0 = blockIdx.y * STEM_TY, nb = blockIdx.z;
-  // constants -> smem
-  for (int i = threadIdx.x; i < int(sizeof(StemConsts) / 4); i += blockDim.x)
-    reinterpret_cast<uint32_t *>(&ks)[i] = reinterpret_cast<const uint32_t *>(k)[i];
-  // halo'd input tile (zero padding outside the image, like float_conv)
+  for (int i = threadIdx.x; i < int(sizeof(StemConsts) / 16); i += blockDim.x)
+    reinterpret_cast<uint4 *>(&ks)[i] = reinterpret_cast<const uint4 *>(k)[i];
   for (int i = threadIdx.x; i < (STEM_TY + 2) * (STEM_TX + 2); i += blockDim.x) {
     const int r = i / (STEM_TX + 2), c = i % (STEM_TX + 2);
     const int iy = y0 - 1 + r, ix = x0 - 1 + c;
@@ -58,51 +75,61 @@ __global__ void __launch_bounds__(STEM_TX *STEM_TY) stem_kernel(
   __syncthreads();
   const int oy = y0 + ty, ox = x0 + tx;
   if (oy >= h || ox >= w) return;
-  float xv[9 * CIN];
+
+  unsigned long long acc[STEM_COUT / 2];
+#pragma unroll
+  for (int j = 0; j < STEM_COUT / 2; ++j) acc[j] = pack2(ks.b[2 * j], ks.b[2 * j + 1]);
   float xmax = 0.f;
   bool finite = true;
 #pragma unroll
-  for (int t = 0; t < 9; ++t)
+  for (int t = 0; t < 9; ++t) {
 #pragma unroll
     for (int ci = 0; ci < CIN; ++ci) {
       const double d = tile[ty + t / 3][tx + t % 3][ci];
       finite &= isfinite(d);
-      xv[t * CIN + ci] = float(d);
-      xmax = fmaxf(xmax, fabsf(float(d)));
-    }
-  uint32_t word[2] = {0u, 0u};
-  for (int o = 0; o < c_out; ++o) {
-    const float *wr = ks.w32 + o * 9 * CIN;
-    float acc = 0.f;
+      const float xf = float(d);
+      xmax = fmaxf(xmax, fabsf(xf));
+      const uint4 *wr = reinterpret_cast<const uint4 *>(ks.w[t * CIN + ci]);
 #pragma unroll
-    for (int i = 0; i < 9 * CIN; ++i) acc = fmaf(xv[i], wr[i], acc);
-    acc += bias64 ? float(__ldg(bias64 + o)) : 0.f;
-    bool bit;
-    const int dir = ks.dir[o];
-    if (dir == 0) {
-      bit = ks.cbit[o] != 0;
-    } else {
-      // |acc32 - acc64| <= (9*CIN + 3) * 2^-23 * (max|x| * sum|w| + |b|)  (generous)
-      const float margin = 1e-5f * (xmax * ks.wabs[o] + ks.babs[o]) + 1e-6f * fabsf(ks.tstar[o]);
-      const float d = acc - ks.tstar[o];
-      if (dir != 2 && finite && fabsf(d) > margin && isfinite(acc)) {
-        bit = dir > 0 ? d > 0.f : d < 0.f;
-      } else {  // exact float64 recomputation in the reference's order
-        double a64 = 0.0;
-        for (int t = 0; t < 9; ++t) {
-          double dot = 0.0;
-          const double *wt = w64 + (int64_t(o) * 9 + t) * CIN;
-          for (int ci = 0; ci < CIN; ++ci)
-            dot = __fma_rn(tile[ty + t / 3][tx + t % 3][ci], __ldg(wt + ci), dot);
-          a64 = __dadd_rn(a64, dot);
-        }
-        if (bias64) a64 = __dadd_rn(a64, __ldg(bias64 + o));
-        const double gm = bn[o], be = bn[c_out + o], mu = bn[2 * c_out + o], sg = bn[3 * c_out + o];
-        const double y = __dadd_rn(__ddiv_rn(__dmul_rn(gm, __dsub_rn(a64, mu)), sg), be);
-        bit = y >= 0.0;
+      for (int q = 0; q < STEM_COUT / 4; ++q) {
+        const uint4 wv = wr[q];
+        acc[2 * q] = ffma2_bcast(xf, (unsigned long long)wv.x | ((unsigned long long)wv.y << 32), acc[2 * q]);
+        acc[2 * q + 1] = ffma2_bcast(xf, (unsigned long long)wv.z | ((unsigned long long)wv.w << 32), acc[2 * q + 1]);
       }
     }
-    word[o >> 5] |= uint32_t(bit) << (o & 31);
+  }
+  uint32_t word[2] = {0u, 0u};
+  unsigned long long unsure = 0ull;
+#pragma unroll
+  for (int j = 0; j < STEM_COUT / 2; ++j) {
+    float a[2];
+    unpack2(acc[j], a[0], a[1]);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int o = 2 * j + e;
+      const float d = a[e] - ks.tstar[o];
+      const float margin = fmaf(xmax, ks.ma[o], ks.mb[o]);
+      const bool sure = finite && fabsf(d) > margin;  // false for NaN / inf margin
+      const bool bit = d * ks.dirf[o] > 0.f;
+      word[o >> 5] |= uint32_t(sure && bit) << (o & 31);
+      unsure |= (unsigned long long)(!sure && o < c_out) << o;
+    }
+  }
+  while (unsure) {  // rare: exact float64 decision in the reference's order
+    const int o = __ffsll(unsure) - 1;
+    unsure &= unsure - 1;
+    double a64 = 0.0;
+    for (int t = 0; t < 9; ++t) {
+      double dot = 0.0;
+      const double *wt = w64 + (int64_t(o) * 9 + t) * CIN;
+      for (int ci = 0; ci < CIN; ++ci)
+        dot = __fma_rn(tile[ty + t / 3][tx + t % 3][ci], __ldg(wt + ci), dot);
+      a64 = __dadd_rn(a64, dot);
+    }
+    if (bias64) a64 = __dadd_rn(a64, __ldg(bias64 + o));
+    const double gm = bn[o], be = bn[c_out + o], mu = bn[2 * c_out + o], sg = bn[3 * c_out + o];
+    const double y = __dadd_rn(__ddiv_rn(__dmul_rn(gm, __dsub_rn(a64, mu)), sg), be);
+    word[o >> 5] |= uint32_t(y >= 0.0) << (o & 31);
   }
   uint32_t *dst = bits + (((int64_t(nb) * h + oy) * w + ox) * out_stride32 + out_offset32);
   if (out_groups == 4 && ((out_stride32 | out_offset32) & 3) == 0) {
@@ -116,32 +143,44 @@ __global__ void __launch_bounds__(STEM_TX *STEM_TY) stem_kernel(
 int stem_prepare(mbu_fconv *fc, const double *w, const double *bias, const double *bn, double eps) {
   fc->stem_fast = 0;
   if (!(fc->kh == 3 && fc->kw == 3 && fc->stride == 1 && fc->pad == 1 && !fc->bits_input && bn &&
-        fc->c_in >= 1 && fc->c_in <= STEM_MAX_CIN && fc->c_out <= STEM_MAX_COUT))
+        fc->c_in >= 1 && fc->c_in <= STEM_MAX_CIN && fc->c_out <= STEM_COUT))
     return MBU_OK;
   StemConsts k{};
   const int co = fc->c_out, ci = fc->c_in;
+  const float inf = INFINITY;
+  for (int o = 0; o < STEM_COUT; ++o) {
+    k.tstar[o] = inf;  // unused channels: never fire, never unsure (masked by c_out)
+    k.dirf[o] = 1.f;
+    k.ma[o] = 0.f;
+    k.mb[o] = 0.f;
+  }
   for (int o = 0; o < co; ++o) {
     double s = 0.0;
     for (int t = 0; t < 9; ++t)
       for (int c = 0; c < ci; ++c) {
         const double v = w[(size_t(o) * 9 + t) * ci + c];
-        k.w32[(o * 9 + t) * ci + c] = float(v);
+        k.w[t * ci + c][o] = float(v);
         s += std::fabs(v);
       }
-    k.wabs[o] = float(s) * 1.001f;
-    k.babs[o] = bias ? float(std::fabs(bias[o])) * 1.001f : 0.f;
+    const double babs = bias ? std::fabs(bias[o]) : 0.0;
+    k.b[o] = bias ? float(bias[o]) : 0.f;
     const double g = bn[o], b = bn[co + o], m = bn[2 * co + o];
     const double sigma = std::sqrt(bn[3 * co + o] + eps);
+    // float32 error of acc <= ~(9*cin + 4) * 2^-23 * (max|x| * sum|w| + |b|): use 1e-5
+    k.ma[o] = float(1e-5 * s * 1.001);
+    k.mb[o] = float(1e-5 * babs * 1.001);
     if (g == 0.0) {
-      k.dir[o] = 0;
-      k.cbit[o] = b >= 0.0;
+      k.dirf[o] = 1.f;
+      k.tstar[o] = b >= 0.0 ? -inf : inf;  // constant: d = +-inf decides (NaN acc -> exact)
     } else {
       const double ts = m - b * sigma / g;
+      k.dirf[o] = g > 0 ? 1.f : -1.f;
       if (!std::isfinite(ts) || std::fabs(ts) > 1e30) {
-        k.dir[o] = 2;  // no usable float32 decision point: always evaluate exactly
+        k.tstar[o] = 0.f;
+        k.mb[o] = inf;  // no usable float32 decision point: always exact
       } else {
-        k.dir[o] = g > 0 ? 1 : -1;
         k.tstar[o] = float(ts);
+        k.mb[o] += float(1e-6 * std::fabs(ts));
       }
     }
   }
@@ -210,10 +249,84 @@ __global__ void __launch_bounds__(256) head_kernel(ActView xb, const int32_t *__
   }
 }
 
+// Byte-table head: with the c_in input channels at lanes 0..c_in-1, the
+// logit is bias + sum over bytes k of T[o][k][byte_k], T holding the signed
+// partial sums of 8 consecutive channel weights (built once on the host, in
+// channel order). Eight shared-memory lookups per pixel replace 64 bit
+// extractions + FMAs. The float64 sum order differs from the reference's BLAS
+// dot only by rounding (|delta| ~ 1e-16 * sum|w|), within the 1e-9 logits
+// tolerance of verify.py:23.
+__global__ void __launch_bounds__(256) head_tab_kernel(ActView xb, const double *__restrict__ tab,
+                                                       const double *__restrict__ bias, int nbytes,
+                                                       int c_out, int64_t pixels,
+                                                       double *__restrict__ logits,
+                                                       uint8_t *__restrict__ mask) {
+  extern __shared__ double ts[];  // [c_out][nbytes][256]
+  for (int i = threadIdx.x; i < c_out * nbytes * 256; i += blockDim.x) ts[i] = tab[i];
+  __syncthreads();
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < pixels;
+       p += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t *xp = xb.base + p * xb.stride + xb.offset;
+    for (int o = 0; o < c_out; ++o) {
+      double acc = 0.0;
+      const double *to = ts + size_t(o) * nbytes * 256;
+      for (int k = 0; k < nbytes; k += 8) {
+        const uint64_t wd = __ldg(xp + (k >> 3));
+        const int kend = min(8, nbytes - k);
+        for (int kk = 0; kk < kend; ++kk)
+          acc = __dadd_rn(acc, to[(k + kk) * 256 + int((wd >> (8 * kk)) & 0xFF)]);
+      }
+      if (bias) acc = __dadd_rn(acc, bias[o]);
+      logits[p * c_out + o] = acc;
+      if (mask) mask[p * c_out + o] = acc >= 0.0 ? 1 : 0;
+    }
+  }
+}
+
+int head_prepare(mbu_fconv *fc, const double *w, const int32_t *lanes) {
+  fc->head_tab = 0;
+  if (!(fc->bits_input && fc->kh == 1 && fc->kw == 1 && fc->stride == 1 && fc->pad == 0)) return MBU_OK;
+  for (int c = 0; c < fc->c_in; ++c)
+    if (lanes[c] != c) return MBU_OK;
+  const int nbytes = (fc->c_in + 7) / 8;
+  const size_t entries = size_t(fc->c_out) * nbytes * 256;
+  if (entries * sizeof(double) > 96 * 1024) return MBU_OK;
+  std::vector<double> tab(entries);
+  for (int o = 0; o < fc->c_out; ++o)
+    for (int k = 0; k < nbytes; ++k)
+      for (int v = 0; v < 256; ++v) {
+        double s = 0.0;
+        for (int i = 0; i < 8 && 8 * k + i < fc->c_in; ++i) {
+          const double wv = w[size_t(o) * fc->c_in + 8 * k + i];
+          s += ((v >> i) & 1) ? wv : -wv;
+        }
+        tab[(size_t(o) * nbytes + k) * 256 + v] = s;
+      }
+  MBU_TRY(check_cuda(cudaMalloc(&fc->d_head_tab, entries * sizeof(double)), "alloc head table"));
+  MBU_TRY(check_cuda(cudaMemcpy(fc->d_head_tab, tab.data(), entries * sizeof(double), cudaMemcpyHostToDevice),
+                     "upload head table"));
+  fc->head_tab = 1;
+  return MBU_OK;
+}
+
 int launch_head_fast(const mbu_fconv *fc, const ActView &xb, int n, int h, int w, double *logits,
                      uint8_t *mask, cudaStream_t st) {
   const int64_t pixels = int64_t(n) * h * w;
   if (pixels == 0) return MBU_OK;
+  if (fc->head_tab) {
+    const int nbytes = (fc->c_in + 7) / 8;
+    const size_t smem = size_t(fc->c_out) * nbytes * 256 * sizeof(double);
+    static bool configured = false;
+    if (!configured) {
+      MBU_TRY(check_cuda(cudaFuncSetAttribute(head_tab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              96 * 1024), "cudaFuncSetAttribute(head)"));
+      configured = true;
+    }
+    const int64_t blocks = std::min<int64_t>((pixels + 255) / 256, 148 * 4);
+    head_tab_kernel<<<unsigned(blocks), 256, smem, st>>>(xb, fc->d_head_tab, fc->d_bias, nbytes,
+                                                         fc->c_out, pixels, logits, mask);
+    return check_launch("head_tab_kernel");
+  }
   const size_t smem = size_t(fc->c_out) * fc->c_in * sizeof(double) + fc->c_in * sizeof(int32_t);
   const int64_t blocks = std::min<int64_t>((pixels + 255) / 256, 148 * 16);
   head_kernel<<<unsigned(blocks), 256, smem, st>>>(xb, fc->d_lanes, fc->d_w, fc->d_bias, fc->c_in,

@@ -537,6 +537,7 @@ int mbu_fconv_create(mbu_fconv **out, int device, int kh, int kw, int stride, in
   }
   if (st == MBU_OK && in_lanes) st = upload(&fc->d_lanes, in_lanes, size_t(c_in), "upload lanes");
   if (st == MBU_OK) st = stem_prepare(fc, weights, bias, bn, eps);
+  if (st == MBU_OK && in_lanes) st = head_prepare(fc, weights, in_lanes);
   if (st != MBU_OK) {
     mbu_fconv_destroy(fc);
     return st;
@@ -552,6 +553,7 @@ int mbu_fconv_destroy(mbu_fconv *fc) {
   cudaFree(fc->d_bn);
   cudaFree(fc->d_lanes);
   cudaFree(fc->d_stem);
+  cudaFree(fc->d_head_tab);
   delete fc;
   return MBU_OK;
 }

@@ -252,9 +252,75 @@ class Engine:
                     self._enqueue()
                 self.graph = g
 
-    def _enqueue(self):
-        self.dm.run(self.image, self.logits, self.mask, self.ws, path=self.path,
+    def _enqueue(self, image=None, logits=None, mask=None):
+        self.dm.run(self.image if image is None else image,
+                    self.logits if logits is None else logits,
+                    self.mask if mask is None else mask, self.ws, path=self.path,
                     stream=torch.cuda.current_stream(self.device))
+
+    # ------------------------------------------------------------ streaming
+    def _ensure_slots(self):
+        """Second set of I/O buffers + graph for copy/compute overlap."""
+        if getattr(self, "_slots", None) is not None:
+            return
+        dev = self.device
+        with torch.cuda.device(dev):
+            slots = [(self.image, self.logits, self.mask, self.graph)]
+            img = torch.zeros(self.shape, dtype=torch.float64, device=dev)
+            lg = torch.empty(self.out_shape, dtype=torch.float64, device=dev)
+            mk = torch.empty(self.out_shape, dtype=torch.uint8, device=dev)
+            g = None
+            if self.graph is not None:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.stream):
+                    self._enqueue(img, lg, mk)
+            slots.append((img, lg, mk, g))
+            self._slots = slots
+            self.h2d = torch.cuda.Stream(dev)
+            self.d2h = torch.cuda.Stream(dev)
+            ev = lambda: torch.cuda.Event()  # noqa: E731
+            self._ev = {k: [ev(), ev()] for k in ("h2d", "comp", "d2h")}
+            self._used = [False, False]
+
+    def run_stream(self, host_images, host_logits, host_masks, steps: int):
+        """Pipelined serving loop over ``steps`` batches.
+
+        Step i copies ``host_images[i % len]`` (pinned) to the device on a
+        copy stream, runs the forward on the compute stream, and copies the
+        logits / mask back on a second copy stream into
+        ``host_logits[i % len]`` / ``host_masks[i % len]``. Two device buffer
+        sets let step i+1's upload and step i-1's download overlap step i's
+        compute. Returns after enqueueing; synchronize on ``self.d2h``.
+        """
+        self._ensure_slots()
+        ev = self._ev
+        for i in range(steps):
+            s = i & 1
+            img, lg, mk, g = self._slots[s]
+            hi = host_images[i % len(host_images)]
+            hl = None if host_logits is None else host_logits[i % len(host_logits)]
+            hm = host_masks[i % len(host_masks)]
+            with torch.cuda.stream(self.h2d):
+                if self._used[s]:
+                    self.h2d.wait_event(ev["comp"][s])  # slot's image consumed
+                img.copy_(hi, non_blocking=True)
+                ev["h2d"][s].record(self.h2d)
+            with torch.cuda.stream(self.stream):
+                self.stream.wait_event(ev["h2d"][s])
+                if self._used[s]:
+                    self.stream.wait_event(ev["d2h"][s])  # slot's outputs downloaded
+                if g is not None:
+                    g.replay()
+                else:
+                    self._enqueue(img, lg, mk)
+                ev["comp"][s].record(self.stream)
+            with torch.cuda.stream(self.d2h):
+                self.d2h.wait_event(ev["comp"][s])
+                if hl is not None:
+                    hl.copy_(lg, non_blocking=True)
+                hm.copy_(mk, non_blocking=True)
+                ev["d2h"][s].record(self.d2h)
+            self._used[s] = True
 
     def run(self):
         with torch.cuda.stream(self.stream):

@@ -142,3 +142,39 @@ def test_path_invariance_at_256(cuda):
     b = mb.runtime.forward(model, image, path=_lib.PATH_POPCOUNT)
     assert np.array_equal(a.mask, b.mask)
     assert np.array_equal(a.logits, b.logits)
+
+
+def test_run_stream_matches_graph_replay(cuda):
+    """The pipelined serving loop returns exactly what a single replay does."""
+    cfg = mb.UNetConfig(height=128, width=256)
+    rng = np.random.default_rng(21)
+    model = mb.build(cfg, mb.live_bundle(cfg, rng))
+    eng = mb.Engine(model, batch=2)
+    imgs = [torch.from_numpy(rng.random(eng.shape)).pin_memory() for _ in range(3)]
+    logits = [torch.empty(eng.out_shape, dtype=torch.float64).pin_memory() for _ in range(3)]
+    masks = [torch.empty(eng.out_shape, dtype=torch.uint8).pin_memory() for _ in range(3)]
+    eng.run_stream(imgs, logits, masks, 3)
+    torch.cuda.synchronize()
+    for i in range(3):
+        eng.image.copy_(imgs[i].to(cuda))
+        eng.run()
+        torch.cuda.synchronize()
+        assert torch.equal(eng.mask.cpu(), masks[i]), i
+        assert torch.equal(eng.logits.cpu(), logits[i]), i
+
+
+def test_fast_endpoints_equal_float64_endpoints_full_width(cuda):
+    """Stem (float32 + exact recheck) and byte-table head against the
+    all-float64 generic kernels on a full 1024x2048 frame."""
+    cfg = mb.UNetConfig(height=1024, width=2048)
+    rng = np.random.default_rng(12)
+    model = mb.build(cfg, mb.live_bundle(cfg, rng))
+    img = rng.random((1, 1024, 2048, 3))
+    a = mb.forward(model, img)
+    _lib.call("mbu_set_option", 1, 1)
+    try:
+        b = mb.forward(model, img)
+    finally:
+        _lib.call("mbu_set_option", 1, 0)
+    assert np.array_equal(a.mask, b.mask)
+    assert np.allclose(a.logits, b.logits, rtol=1e-12, atol=1e-12)
