@@ -18,6 +18,14 @@
 // layers.py:270) or 0 (pad_mode "zero", equal to the reference's weight-sum
 // correction, layers.py:306-312).
 //
+// Fused threshold (layers.py:508-522) without a compare per value: before a
+// tile's first MMA the epilogue warps tcgen05.st a per-column bias into the
+// accumulator, and columns with code DIR_LE carry negated weights, so TMEM
+// ends up holding  acc' = s*(acc - T)  (s = +1 for DIR_GE, -1 for DIR_LE;
+// constant codes get a bias beyond the accumulator range). The output bit is
+// then just "acc' >= 0", i.e. the complement of the sign bit, and the true
+// accumulator (trace mode) is recovered as acc = s*acc' + T.
+//
 // Implicit GEMM without im2col: the producers expand a halo'd strip of input
 // rows (R+2 rows x TW+2 columns) ONCE per 32-channel chunk; the A operand of
 // tap (dy, dx) is that same strip with the UMMA descriptor's start address
@@ -25,9 +33,9 @@
 // 16 B, so any pixel offset is a legal start). Nine MMAs read one strip.
 //
 // Persistent, warp-specialised (512 threads, one CTA per SM):
-//   warps 0-7   epilogue: TMEM -> fused threshold + bit-pack -> HBM
-//               (warp w drains TMEM lanes 32*(w%4).. of M-blocks b = w/4 mod 2)
-//   warps 8-13  producers: packed bits -> s8 strips (batched loads)
+//   warps 0-7   epilogue: bias -> TMEM, TMEM -> sign bits -> HBM. The two
+//               warps of a TMEM lane quarter split M-blocks (or column runs)
+//   warps 8-13  producers: packed bits -> s8 strips, one stage of lookahead
 //   warp 14     one lane issues tcgen05.mma; owns TMEM alloc/dealloc
 //   warp 15     one lane streams pre-arranged weight stages (cp.async.bulk)
 // Smem stages cycle through full/empty mbarriers; two TMEM accumulator
@@ -58,7 +66,7 @@ constexpr int TMEM_COLS = 512;  // two buffers
 constexpr int MAX_STAGES = 8;
 constexpr int SMEM_HEADER = 1024;
 constexpr int MIN_SMEM = 120 * 1024;  // > half an SM: exactly one CTA (and TMEM owner) per SM
-constexpr int PROD_ITEMS = 8;  // strip rows per producer thread per stage (Q <= 8 * 192)
+constexpr int PROD_ITEMS = 8;         // strip rows per producer thread per stage (Q <= 8*192)
 
 struct Params {
   const uint32_t *x32;
@@ -81,7 +89,8 @@ struct Params {
   int32_t *acc;
   uint32_t *bits;
   int out_stride32, out_off32, out_groups;
-  const int2 *thr2;         // per column: fires <=> m * acc >= t
+  const int32_t *col_bias;  // per GEMM column: TMEM init value
+  const int32_t *col_sgn;   // per GEMM column: +-1 (acc = sgn * acc' + T, T = -sgn * bias)
 };
 
 // ----------------------------------------------------------------- PTX glue
@@ -139,13 +148,12 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   d |= uint64_t(1) << 46;
   return d;
 }
-__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
-                                        uint32_t accumulate) {
+__device__ __forceinline__ void umma_i8_acc(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 p, 1, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      "l"(a), "l"(b), "r"(idesc)
       : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
@@ -153,6 +161,12 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
                    bar)
                : "memory");
 }
+#define MBU_R32(v)                                                                             \
+  "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),      \
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),        \
+      "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),      \
+      "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),      \
+      "r"(v[29]), "r"(v[30]), "r"(v[31])
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -166,8 +180,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void named_bar_sync(int id, int threads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      MBU_R32(v)
+      : "memory");
 }
 
 // 4 activation bits -> 4 s8 lanes of +-1 (bit 1 -> 0x01, bit 0 -> 0xFF)
@@ -199,6 +218,25 @@ __device__ __forceinline__ Tile decode_tile(const Params &p, int t) {
 }
 __device__ __forceinline__ int block_q0(const Params &p, int b) {
   return p.row_mode ? (b + p.halo) * p.P + p.halo : p.halo * p.P + p.halo + BLOCK_M * b;
+}
+
+// Epilogue work split. Every (M-block, column run) of a tile is handled by
+// one of the two warps sharing a TMEM lane quarter: by block parity when the
+// tile has >= 2 blocks, else by run parity. A run is a maximal range of
+// 32-column groups that lands in one output pixel (a tconv tap).
+struct Run {
+  int g, len, tap, o0;
+};
+__device__ __forceinline__ Run run_at(const Params &p, int jt, int g, int groups, bool tconv) {
+  Run r;
+  r.g = g;
+  const int j0 = jt + 32 * g;
+  const int span = tconv ? p.c_out_pad : p.n_gemm;
+  r.tap = tconv ? j0 / p.c_out_pad : 0;
+  r.o0 = j0 - r.tap * p.c_out_pad;
+  r.len = min(groups - g, (span - r.o0) / 32);
+  if (j0 >= p.n_gemm) r.len = 0;
+  return r;
 }
 
 // ------------------------------------------------------------------ kernel
@@ -241,38 +279,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
   const uint32_t tmem = *tmem_slot;
 
   if (warp >= PROD_WARP0 && warp < MMA_WARP) {
-    // ============ producers: packed bits -> s8 strips ============
-    // One-stage lookahead: the global loads of stage g+1 are in flight while
-    // stage g is expanded into shared memory (hides HBM/L2 latency).
+    // ============ producers: packed bits -> s8 strips (one stage lookahead) ============
     const int pt = threadIdx.x - PROD_WARP0 * 32;
     const uint32_t oob = p.zero_pad ? 0u : 0xFFFFFFFFu;
     const int strip_rows = p.R + 2 * p.halo;
-    auto in_bounds = [&](const Tile &tl, int q) -> bool {
-      const int rr = int(__umulhi(uint32_t(q), p.p_magic));
-      const int cc = q - rr * p.P;
-      const int iy = tl.y0 - p.halo + rr;
-      const int ix = tl.x0 - p.halo + cc;
-      return q < p.Q && rr < strip_rows && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w;
-    };
-    auto load_stage = [&](int t, int k, uint32_t (&wd)[PROD_ITEMS]) {
+    auto load_stage = [&](int t, int k, uint32_t (&wd)[PROD_ITEMS]) -> uint32_t {
       const Tile tl = decode_tile(p, t);
       const int cw = __ldg(p.chunk_word + k);
+      uint32_t inb = 0;
 #pragma unroll
       for (int j = 0; j < PROD_ITEMS; ++j) {
         const int q = pt + j * PROD_THREADS;
+        const int rr = int(__umulhi(uint32_t(q), p.p_magic));
+        const int iy = tl.y0 - p.halo + rr;
+        const int ix = tl.x0 - p.halo + (q - rr * p.P);
         wd[j] = 0u;
-        if (in_bounds(tl, q)) {
-          const int rr = int(__umulhi(uint32_t(q), p.p_magic));
-          const int iy = tl.y0 - p.halo + rr;
-          const int ix = tl.x0 - p.halo + (q - rr * p.P);
+        if (q < p.Q && rr < strip_rows && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w) {
           const int64_t pix = (int64_t(tl.nb) * p.h + iy) * p.w + ix;
           wd[j] = __ldg(p.x32 + pix * p.x_stride32 + p.x_off32 + cw);
+          inb |= 1u << j;
         }
       }
+      return inb;
     };
     uint32_t cur[PROD_ITEMS], nxt[PROD_ITEMS];
     int t = blockIdx.x, k = 0;
-    if (t < p.num_tiles) load_stage(t, 0, cur);
+    uint32_t inb_cur = 0, inb_nxt = 0;
+    if (t < p.num_tiles) inb_cur = load_stage(t, 0, cur);
     int k_global = 0;
     while (t < p.num_tiles) {
       int tn = t, kn = k + 1;
@@ -280,19 +313,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         kn = 0;
         tn += gridDim.x;
       }
-      if (tn < p.num_tiles) load_stage(tn, kn, nxt);
+      if (tn < p.num_tiles) inb_nxt = load_stage(tn, kn, nxt);
       const int s = k_global % S;
       const int u = k_global / S;
       if (u > 0) mbar_wait(smem_u32(&empty[s]), (u - 1) & 1);
       const uint32_t a0 = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
       const uint32_t a1 = a0 + p.Q * 16;
-      const Tile tl = decode_tile(p, t);
 #pragma unroll
       for (int j = 0; j < PROD_ITEMS; ++j) {
         const int q = pt + j * PROD_THREADS;
         if (q < p.Q) {
           const uint32_t b = cur[j];
-          if (in_bounds(tl, q)) {
+          if ((inb_cur >> j) & 1) {
             sts128(a0 + q * 16, expand4(b & 0xF), expand4((b >> 4) & 0xF),
                    expand4((b >> 8) & 0xF), expand4((b >> 12) & 0xF));
             sts128(a1 + q * 16, expand4((b >> 16) & 0xF), expand4((b >> 20) & 0xF),
@@ -307,12 +339,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       mbar_arrive(smem_u32(&full[s]));
 #pragma unroll
       for (int j = 0; j < PROD_ITEMS; ++j) cur[j] = nxt[j];
+      inb_cur = inb_nxt;
       t = tn;
       k = kn;
       ++k_global;
     }
   } else if (warp == MMA_WARP) {
-    // ============ single-thread MMA issue ============
+    // ============ single-thread MMA issue (accumulators pre-loaded with bias) ============
     if (lane == 0) {
       const uint32_t sbo = 128;
       const uint32_t a_lbo = uint32_t(p.Q) * 16;
@@ -320,7 +353,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       int k_global = 0, it = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         const int ab = it & 1;
-        if (it >= 2) mbar_wait(smem_u32(&acc_empty[ab]), ((it >> 1) - 1) & 1);
+        mbar_wait(smem_u32(&acc_empty[ab]), (it >> 1) & 1);
         tc_fence_after();
         const uint32_t d0 = tmem + uint32_t(ab * ACC_COLS);
         for (int k = 0; k < p.kc; ++k, ++k_global) {
@@ -336,7 +369,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
               const int off = TAPS == 9 ? (tap / 3 - 1) * p.P + (tap % 3 - 1) : 0;
               const uint64_t ad = umma_desc(a_s + uint32_t(q0 + off) * 16, a_lbo, sbo);
               const uint64_t bd = umma_desc(b_s + uint32_t(tap * p.n_tile * 32), b_lbo, sbo);
-              umma_i8(d0 + uint32_t(b * p.n_tile), ad, bd, p.idesc, (k | tap) != 0);
+              umma_i8_acc(d0 + uint32_t(b * p.n_tile), ad, bd, p.idesc);
             }
           }
           umma_commit(smem_u32(&empty[s]));
@@ -365,78 +398,100 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     }
     __syncwarp();
   } else {
-    // ============ epilogue: TMEM -> threshold -> packed bits / int32 acc ============
+    // ============ epilogue ============
     const int quarter = warp & 3;
     const int half = warp >> 2;
     const int m = quarter * 32 + lane;
     const int groups = p.n_tile / 32;
+    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
+    // bias -> TMEM for every (block, run) unit this warp owns in tile t
+    auto init_buffer = [&](int t, int ab) {
+      if (t < p.num_tiles) {
+        const int jt = (t % p.n_tiles) * p.n_tile;
+        int ri = 0;
+        for (int g = 0; g < groups; ++ri) {
+          const Run rn = run_at(p, jt, g, groups, TCONV);
+          if (rn.len == 0) break;
+          for (int b = 0; b < p.MB; ++b) {
+            if ((p.MB >= 2 ? b : ri) % 2 != half) continue;
+            for (int gg = rn.g; gg < rn.g + rn.len; ++gg) {
+              uint32_t v[32];
+              const int4 *src = reinterpret_cast<const int4 *>(p.col_bias + jt + 32 * gg);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int4 q4 = __ldg(src + i);
+                v[4 * i] = q4.x;
+                v[4 * i + 1] = q4.y;
+                v[4 * i + 2] = q4.z;
+                v[4 * i + 3] = q4.w;
+              }
+              tmem_st32(lane_base + uint32_t(ab * ACC_COLS + b * p.n_tile + gg * 32), v);
+            }
+          }
+          g += rn.len;
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      tc_fence_before();
+      mbar_arrive(smem_u32(&acc_empty[ab]));
+    };
+    init_buffer(blockIdx.x, 0);
+    init_buffer(blockIdx.x + gridDim.x, 1);
     int it = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
       const int ab = it & 1;
       const Tile tl = decode_tile(p, t);
       mbar_wait(smem_u32(&acc_full[ab]), (it >> 1) & 1);
       tc_fence_after();
-      const uint32_t lane_addr = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(ab * ACC_COLS);
       const int jt = tl.nt * p.n_tile;
-      const int span = TCONV ? p.c_out_pad : p.n_gemm;  // GEMM columns per output pixel
-      for (int b = half; b < p.MB; b += 2) {
-        const int q = block_q0(p, b) + m;
-        const int rq = int(__umulhi(uint32_t(q), p.p_magic));
-        const int r = rq - p.halo;
-        const int c = q - rq * p.P - p.halo;
-        const int yy = tl.y0 + r, xx = tl.x0 + c;
-        const bool valid = r >= 0 && r < p.R && c >= 0 && c < p.TW && yy < p.h && xx < p.w;
-        // walk the tile's 32-column groups in runs that share one output pixel
-        int g = 0;
-        while (g < groups) {
-          const int j0 = jt + 32 * g;
-          if (j0 >= p.n_gemm) break;
-          const int tap = TCONV ? j0 / p.c_out_pad : 0;
-          const int o0 = j0 - tap * p.c_out_pad;
-          const int run = min(groups - g, (span - o0) / 32);
-          const int oy = TCONV ? yy * p.tconv_s + tap / p.tconv_s : yy;
-          const int ox = TCONV ? xx * p.tconv_s + tap % p.tconv_s : xx;
+      int ri = 0;
+      for (int g = 0; g < groups; ++ri) {
+        const Run rn = run_at(p, jt, g, groups, TCONV);
+        if (rn.len == 0) break;
+        for (int b = 0; b < p.MB; ++b) {
+          if ((p.MB >= 2 ? b : ri) % 2 != half) continue;
+          const int q = block_q0(p, b) + m;
+          const int rq = int(__umulhi(uint32_t(q), p.p_magic));
+          const int r = rq - p.halo;
+          const int c = q - rq * p.P - p.halo;
+          const int yy = tl.y0 + r, xx = tl.x0 + c;
+          const bool valid = r >= 0 && r < p.R && c >= 0 && c < p.TW && yy < p.h && xx < p.w;
+          const int oy = TCONV ? yy * p.tconv_s + rn.tap / p.tconv_s : yy;
+          const int ox = TCONV ? xx * p.tconv_s + rn.tap % p.tconv_s : xx;
           const int64_t opix = (int64_t(tl.nb) * p.ho + oy) * p.wo + ox;
           uint32_t w8[8];
 #pragma unroll
           for (int rr = 0; rr < 8; ++rr) {
             w8[rr] = 0u;
-            if (rr < run) {
+            if (rr < rn.len) {
               uint32_t v[32];
-              tmem_ld32(lane_addr + uint32_t(b * p.n_tile + (g + rr) * 32), v);
-              const int2 *th = p.thr2 + j0 + 32 * rr;
-              uint32_t wd = 0;
+              const int gg = rn.g + rr;
+              tmem_ld32(lane_base + uint32_t(ab * ACC_COLS + b * p.n_tile + gg * 32), v);
+              uint32_t sgn = 0;
 #pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                const int2 e = __ldg(th + i);
-                wd |= uint32_t(e.x * int(v[i]) >= e.y) << i;
-              }
-              w8[rr] = wd;
+              for (int i = 0; i < 32; ++i) sgn |= (v[i] >> 31) << i;
+              w8[rr] = ~sgn;  // bit = acc' >= 0
               if (p.acc && valid) {
-                const int oc = o0 + 32 * rr;
+                const int oc = rn.o0 + 32 * rr;
+                const int jc = jt + 32 * gg;
                 int32_t *dst = p.acc + opix * p.c_out + oc;
-                if (oc + 32 <= p.c_out && (p.c_out % 4) == 0) {
-#pragma unroll
-                  for (int i = 0; i < 32; i += 4)
-                    *reinterpret_cast<int4 *>(dst + i) =
-                        make_int4(int(v[i]), int(v[i + 1]), int(v[i + 2]), int(v[i + 3]));
-                } else {
-                  for (int i = 0; i < 32; ++i)
-                    if (oc + i < p.c_out) dst[i] = int(v[i]);
+                for (int i = 0; i < 32 && oc + i < p.c_out; ++i) {
+                  const int s = __ldg(p.col_sgn + jc + i), bias = __ldg(p.col_bias + jc + i);
+                  dst[i] = s * (int(v[i]) - bias);
                 }
               }
             }
           }
           if (valid && p.bits) {
-            // write the run; when it ends the pixel's channels, append the
+            // write the run; when it ends the pixel's channels append the
             // zero pad groups of the 128-lane block
             uint32_t *dst = p.bits + opix * p.out_stride32 + p.out_off32;
-            const int g0 = o0 / 32;
-            const int wend = (g0 + run == p.c_out_pad / 32) ? p.out_groups : g0 + run;
+            const int g0 = rn.o0 / 32;
+            const int wend = (g0 + rn.len == p.c_out_pad / 32) ? p.out_groups : g0 + rn.len;
             int gg = g0;
             while (gg < wend) {
               const int i = gg - g0;
-              auto wv = [&](int ii) { return ii < run ? w8[ii & 7] : 0u; };
+              auto wv = [&](int ii) { return ii < rn.len ? w8[ii & 7] : 0u; };
               if ((gg & 3) == 0 && gg + 4 <= wend) {
                 *reinterpret_cast<uint4 *>(dst + gg) = make_uint4(wv(i), wv(i + 1), wv(i + 2), wv(i + 3));
                 gg += 4;
@@ -449,11 +504,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
               }
             }
           }
-          g += run;
         }
+        g += rn.len;
       }
-      tc_fence_before();
-      mbar_arrive(smem_u32(&acc_empty[ab]));
+      // buffer drained: re-arm it with the bias of the tile that reuses it
+      init_buffer(t + 2 * gridDim.x, ab);
     }
   }
 
@@ -496,8 +551,6 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
   const int s2 = cv->transposed ? cv->stride * cv->stride : 1;
   const int c_out_pad = (cv->c_out + 31) / 32 * 32;
   const int n_gemm = s2 * c_out_pad;
-  // An N tile must never straddle two output pixels (tconv taps): pick the
-  // largest width <= 128 that divides the per-pixel span when it exceeds 128.
   // N tile: conv -> up to 128 columns (MB = 2 blocks of 128 pixels share each
   // weight stage). tconv -> whole taps when they fit in 256 columns so the A
   // strip is expanded once for all s*s taps, else 128-column slices of a tap.
@@ -508,6 +561,37 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
   else if (c_out_pad % 64 == 0) n_tile = 64;
   else n_tile = 32;
   const int n_tiles = (n_gemm + n_tile - 1) / n_tile;
+  const int n_cols = n_tiles * n_tile;
+
+  // per GEMM column: threshold folded into (weight sign, TMEM bias)
+  std::vector<int32_t> col_bias(size_t(n_cols) + 32, 0), col_sgn(size_t(n_cols) + 32, 1);
+  std::vector<int8_t> col_neg(size_t(n_cols), 0);
+  const int kmax = taps * lpp + 1;  // > max |acc|
+  if (cv->has_threshold) {
+    std::vector<int32_t> t(static_cast<size_t>(c_out_pad), 0);
+    std::vector<uint8_t> c(static_cast<size_t>(c_out_pad), 2);
+    MBU_TRY(check_cuda(cudaMemcpy(t.data(), cv->d_thr, t.size() * 4, cudaMemcpyDeviceToHost), "thr"));
+    MBU_TRY(check_cuda(cudaMemcpy(c.data(), cv->d_codes, c.size(), cudaMemcpyDeviceToHost), "codes"));
+    for (int j = 0; j < n_cols; ++j) {
+      int code = 2, T = 0;
+      if (j < n_gemm) {
+        const int o = cv->transposed ? j % c_out_pad : j;
+        code = c[o];
+        T = t[o];
+      }
+      // out-of-range thresholds are constants over the reachable accumulators
+      if (code == 0 && T <= -kmax) code = 3;
+      if (code == 0 && T >= kmax) code = 2;
+      if (code == 1 && T >= kmax) code = 3;
+      if (code == 1 && T <= -kmax) code = 2;
+      switch (code) {
+        case 0: col_bias[j] = -T; col_sgn[j] = 1; break;                 // acc - T >= 0
+        case 1: col_bias[j] = T; col_sgn[j] = -1; col_neg[j] = 1; break;  // T - acc >= 0
+        case 3: col_bias[j] = kmax; col_sgn[j] = 1; break;               // always >= 0
+        default: col_bias[j] = -2 * kmax; col_sgn[j] = 1; break;         // always < 0
+      }
+    }
+  }
   const size_t b_stage = size_t(taps) * n_tile * 32;
   std::vector<int8_t> b(size_t(n_tiles) * kc * b_stage, 0);
   const int ptaps = cv->kh * cv->kw;  // taps in the reference plane layout
@@ -535,7 +619,7 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
               int v;
               if (neg) v = bit(pos, o, ptap, L) - bit(neg, o, ptap, L);
               else v = real[L] ? 2 * bit(pos, o, ptap, L) - 1 : 0;
-              dst[i] = int8_t(v);
+              dst[i] = int8_t(col_neg[j] ? -v : v);
             }
           }
   MBU_TRY(check_cuda(cudaMalloc(&cv->d_b, b.size()), "alloc tc weights"));
@@ -544,34 +628,15 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
   MBU_TRY(check_cuda(cudaMemcpy(cv->d_chunk_word, chunk_word.data(), kc * sizeof(int32_t),
                                 cudaMemcpyHostToDevice),
                      "upload chunk map"));
-  // per GEMM column threshold in "m * acc >= t" form
-  std::vector<int2> thr2(size_t(n_tiles) * n_tile + 32, make_int2(0, 1));
-  if (cv->has_threshold) {
-    std::vector<int32_t> t(static_cast<size_t>(c_out_pad), 0);
-    std::vector<uint8_t> c(static_cast<size_t>(c_out_pad), 2);
-    MBU_TRY(check_cuda(cudaMemcpy(t.data(), cv->d_thr, t.size() * 4, cudaMemcpyDeviceToHost), "thr"));
-    MBU_TRY(check_cuda(cudaMemcpy(c.data(), cv->d_codes, c.size(), cudaMemcpyDeviceToHost), "codes"));
-    const int lim = 1 << 30;
-    for (int j = 0; j < n_gemm; ++j) {
-      const int o = cv->transposed ? j % c_out_pad : j;
-      const int T = t[o];
-      int2 e = make_int2(0, 1);  // never fires
-      switch (c[o]) {
-        case 0: e = T <= -lim ? make_int2(0, 0) : T > lim ? make_int2(0, 1) : make_int2(1, T); break;
-        case 1: e = T >= lim ? make_int2(0, 0) : T < -lim ? make_int2(0, 1) : make_int2(-1, -T); break;
-        case 3: e = make_int2(0, 0); break;
-        default: break;
-      }
-      thr2[j] = e;
-    }
-  }
-  MBU_TRY(check_cuda(cudaMalloc(&cv->d_thr2, thr2.size() * sizeof(int2)), "alloc thr2"));
-  MBU_TRY(check_cuda(cudaMemcpy(cv->d_thr2, thr2.data(), thr2.size() * sizeof(int2), cudaMemcpyHostToDevice),
-                     "upload thr2"));
+  std::vector<int32_t> cols(col_bias);
+  cols.insert(cols.end(), col_sgn.begin(), col_sgn.end());
+  MBU_TRY(check_cuda(cudaMalloc(&cv->d_thr2, cols.size() * sizeof(int32_t)), "alloc column bias"));
+  MBU_TRY(check_cuda(cudaMemcpy(cv->d_thr2, cols.data(), cols.size() * sizeof(int32_t), cudaMemcpyHostToDevice),
+                     "upload column bias"));
   cv->taps = taps;
   cv->kc = kc;
   cv->n_gemm = n_gemm;
-  cv->n_pad = n_gemm;
+  cv->n_pad = n_cols;
   cv->c_out_pad = c_out_pad;
   cv->n_tile = n_tile;
   cv->n_tiles = n_tiles;
@@ -665,7 +730,8 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   p.out_stride32 = out_stride * 2;
   p.out_off32 = out_offset * 2;
   p.out_groups = cv->out_wpp * 2;
-  p.thr2 = reinterpret_cast<const int2 *>(cv->d_thr2);
+  p.col_bias = static_cast<const int32_t *>(cv->d_thr2);
+  p.col_sgn = p.col_bias + cv->n_pad + 32;
   const int64_t tiles = int64_t(x.n) * p.row_tiles * p.col_tiles * p.n_tiles;
   if (tiles == 0) return MBU_OK;
   if (tiles > 0x7FFFFFFF) return fail(MBU_ERR_SHAPE, "tcgen05 conv grid too large");
