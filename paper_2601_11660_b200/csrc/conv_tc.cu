@@ -10,21 +10,25 @@
 // over packed lanes. Both equal the integer dot product
 //   acc = sum_lanes a * w,  a = 2a'-1 in {-1,+1},  w in {-1,0,+1}
 // where w = pos - neg (masked) or 2b'-1 on real lanes and 0 on pad lanes
-// (binary). This kernel evaluates exactly that sum on the 5th-gen tensor
-// cores with kind::i8 (s8 x s8 -> s32 in TMEM): weights are expanded once at
-// upload into s8, activations stay bit-packed in HBM and are expanded to s8
-// +-1 in shared memory by producer warps. |acc| <= 9*c_in < 2^31: exact.
-// Out-of-bounds taps read -1 (pad_mode "neg_one", the zero-word gather of
-// layers.py:270) or 0 (pad_mode "zero", equal to the reference's weight-sum
-// correction, layers.py:306-312).
+// (binary). The tensor cores evaluate it exactly with kind::i8 (s32
+// accumulation in TMEM; |acc| <= 9*c_in):
+//   * pad_mode "neg_one" (out-of-bounds taps read -1, the zero-word gather of
+//     layers.py:270): A holds the raw bits a' in {0,1} as u8 and
+//     acc = 2*D - W with D = sum a'*w and W = sum w over the column (an
+//     out-of-bounds tap has a' = 0, i.e. -1, consistently);
+//   * pad_mode "zero" (out-of-bounds taps read 0, equal to the reference's
+//     weight-sum correction, layers.py:306-312): A holds a in {-1,+1} as s8
+//     (0 out of bounds) and acc = D.
+// Weights are expanded once at upload into s8; activations stay bit-packed
+// in HBM and are expanded in shared memory by producer warps.
 //
 // Fused threshold (layers.py:508-522) without a compare per value: before a
 // tile's first MMA the epilogue warps tcgen05.st a per-column bias into the
-// accumulator, and columns with code DIR_LE carry negated weights, so TMEM
-// ends up holding  acc' = s*(acc - T)  (s = +1 for DIR_GE, -1 for DIR_LE;
-// constant codes get a bias beyond the accumulator range). The output bit is
-// then just "acc' >= 0", i.e. the complement of the sign bit, and the true
-// accumulator (trace mode) is recovered as acc = s*acc' + T.
+// accumulator, and DIR_LE columns carry negated weights, so TMEM ends up
+// holding D' = s*(D - D_T) with D_T the smallest (GE) / largest (LE) D that
+// fires; constant codes get a bias beyond the reachable range. The output bit
+// is then "D' >= 0", the complement of the sign bit. Trace mode recovers
+// acc = f*(s*(D' - bias)) - W (f = 2 for u8 activations, 1 for s8).
 //
 // Implicit GEMM without im2col: the producers expand a halo'd strip of input
 // rows (R+2 rows x TW+2 columns) ONCE per 32-channel chunk; the A operand of
@@ -32,12 +36,12 @@
 // moved by (dy-1)*P + (dx-1) rows of 16 B (K-major, no swizzle: one row is
 // 16 B, so any pixel offset is a legal start). Nine MMAs read one strip.
 //
-// Persistent, warp-specialised (512 threads, one CTA per SM):
+// Persistent, warp-specialised (576 threads, one CTA per SM):
 //   warps 0-7   epilogue: bias -> TMEM, TMEM -> sign bits -> HBM. The two
 //               warps of a TMEM lane quarter split M-blocks (or column runs)
-//   warps 8-13  producers: packed bits -> s8 strips, one stage of lookahead
-//   warp 14     one lane issues tcgen05.mma; owns TMEM alloc/dealloc
-//   warp 15     one lane streams pre-arranged weight stages (cp.async.bulk)
+//   warps 8-15  producers: packed bits -> u8/s8 strips, one stage lookahead
+//   warp 16     one lane issues tcgen05.mma; owns TMEM alloc/dealloc
+//   warp 17     one lane streams pre-arranged weight stages (cp.async.bulk)
 // Smem stages cycle through full/empty mbarriers; two TMEM accumulator
 // buffers (2 x 256 columns) let the epilogue of tile i overlap the MMAs of
 // tile i+1.
@@ -54,7 +58,7 @@ namespace tc {
 
 constexpr int BLOCK_M = 128;
 constexpr int NUM_EPI_WARPS = 8;
-constexpr int NUM_PROD_WARPS = 6;
+constexpr int NUM_PROD_WARPS = 8;
 constexpr int PROD_WARP0 = NUM_EPI_WARPS;
 constexpr int MMA_WARP = PROD_WARP0 + NUM_PROD_WARPS;
 constexpr int BLOAD_WARP = MMA_WARP + 1;
@@ -64,9 +68,10 @@ constexpr int EPI_THREADS = NUM_EPI_WARPS * 32;
 constexpr int ACC_COLS = 256;   // one accumulator buffer
 constexpr int TMEM_COLS = 512;  // two buffers
 constexpr int MAX_STAGES = 8;
+constexpr int MAX_CHUNKS = 64;  // 32-lane chunks per pixel (2048 lanes)
 constexpr int SMEM_HEADER = 1024;
 constexpr int MIN_SMEM = 120 * 1024;  // > half an SM: exactly one CTA (and TMEM owner) per SM
-constexpr int PROD_ITEMS = 8;         // strip rows per producer thread per stage (Q <= 8*192)
+constexpr int PROD_ITEMS = 6;         // strip rows per producer thread per stage (Q <= 6*256)
 
 struct Params {
   const uint32_t *x32;
@@ -75,7 +80,7 @@ struct Params {
   int halo, P, Q, R, TW, row_mode, MB;
   uint32_t p_magic;         // ceil(2^32 / P): q / P == umulhi(q, p_magic) for q < 2^16
   int col_tiles, row_tiles, n_tiles, num_tiles;
-  int zero_pad;
+  int u8_act;               // 1: A = bits as u8 {0,1} (neg_one); 0: s8 {-1,0,+1} (zero pad)
   int kc;
   const int32_t *chunk_word;
   const int8_t *b;
@@ -90,7 +95,8 @@ struct Params {
   uint32_t *bits;
   int out_stride32, out_off32, out_groups;
   const int32_t *col_bias;  // per GEMM column: TMEM init value
-  const int32_t *col_sgn;   // per GEMM column: +-1 (acc = sgn * acc' + T, T = -sgn * bias)
+  const int32_t *col_sgn;   // per GEMM column: +-1
+  const int32_t *col_w;     // per GEMM column: W (u8 mode) or 0
 };
 
 // ----------------------------------------------------------------- PTX glue
@@ -189,11 +195,10 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       : "memory");
 }
 
-// 4 activation bits -> 4 s8 lanes of +-1 (bit 1 -> 0x01, bit 0 -> 0xFF)
-__device__ __forceinline__ uint32_t expand4(uint32_t nib) {
-  const uint32_t spread = (nib * 0x00204081u) & 0x01010101u;
-  return ~(spread * 0xFEu);
-}
+// 4 activation bits -> 4 bytes. u8 mode: bit -> 0x00/0x01. s8 mode: bit 1 ->
+// 0x01 (+1), bit 0 -> 0xFF (-1).
+__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
+__device__ __forceinline__ uint32_t pm4(uint32_t nib) { return ~(spread4(nib) * 0xFEu); }
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
                                        uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
@@ -248,6 +253,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
   uint64_t *acc_full = empty + MAX_STAGES;
   uint64_t *acc_empty = acc_full + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
+  int32_t *chunk_s = reinterpret_cast<int32_t *>(smem + 512);  // MAX_CHUNKS words
   uint8_t *a_base = smem + SMEM_HEADER;
   uint8_t *b_base = a_base + size_t(p.stages) * p.a_stage_bytes;
 
@@ -266,6 +272,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int i = threadIdx.x; i < p.kc; i += blockDim.x) chunk_s[i] = p.chunk_word[i];
   if (warp == MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
@@ -279,32 +286,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
   const uint32_t tmem = *tmem_slot;
 
   if (warp >= PROD_WARP0 && warp < MMA_WARP) {
-    // ============ producers: packed bits -> s8 strips (one stage lookahead) ============
+    // ============ producers: packed bits -> u8/s8 strips ============
+    // Per tile, each thread caches the 32-bit word offset of its strip rows
+    // (and an in-bounds mask); per stage it only adds the chunk's word index.
+    // The loads of stage g+1 are issued before stage g is expanded.
     const int pt = threadIdx.x - PROD_WARP0 * 32;
-    const uint32_t oob = p.zero_pad ? 0u : 0xFFFFFFFFu;
     const int strip_rows = p.R + 2 * p.halo;
-    auto load_stage = [&](int t, int k, uint32_t (&wd)[PROD_ITEMS]) -> uint32_t {
+    int off[PROD_ITEMS];
+    uint32_t inb = 0;
+    int cached_t = -1;
+    auto tile_offsets = [&](int t) {
       const Tile tl = decode_tile(p, t);
-      const int cw = __ldg(p.chunk_word + k);
-      uint32_t inb = 0;
+      inb = 0;
 #pragma unroll
       for (int j = 0; j < PROD_ITEMS; ++j) {
         const int q = pt + j * PROD_THREADS;
         const int rr = int(__umulhi(uint32_t(q), p.p_magic));
         const int iy = tl.y0 - p.halo + rr;
         const int ix = tl.x0 - p.halo + (q - rr * p.P);
-        wd[j] = 0u;
-        if (q < p.Q && rr < strip_rows && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w) {
-          const int64_t pix = (int64_t(tl.nb) * p.h + iy) * p.w + ix;
-          wd[j] = __ldg(p.x32 + pix * p.x_stride32 + p.x_off32 + cw);
-          inb |= 1u << j;
-        }
+        off[j] = ((tl.nb * p.h + iy) * p.w + ix) * p.x_stride32 + p.x_off32;
+        if (q < p.Q && rr < strip_rows && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w) inb |= 1u << j;
       }
-      return inb;
+      cached_t = t;
     };
     uint32_t cur[PROD_ITEMS], nxt[PROD_ITEMS];
-    int t = blockIdx.x, k = 0;
     uint32_t inb_cur = 0, inb_nxt = 0;
+    auto load_stage = [&](int t, int k, uint32_t (&wd)[PROD_ITEMS]) -> uint32_t {
+      if (t != cached_t) tile_offsets(t);
+      const int cw = chunk_s[k];
+#pragma unroll
+      for (int j = 0; j < PROD_ITEMS; ++j) wd[j] = ((inb >> j) & 1) ? __ldg(p.x32 + off[j] + cw) : 0u;
+      return inb;
+    };
+    int t = blockIdx.x, k = 0;
     if (t < p.num_tiles) inb_cur = load_stage(t, 0, cur);
     int k_global = 0;
     while (t < p.num_tiles) {
@@ -325,13 +339,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         if (q < p.Q) {
           const uint32_t b = cur[j];
           if ((inb_cur >> j) & 1) {
-            sts128(a0 + q * 16, expand4(b & 0xF), expand4((b >> 4) & 0xF),
-                   expand4((b >> 8) & 0xF), expand4((b >> 12) & 0xF));
-            sts128(a1 + q * 16, expand4((b >> 16) & 0xF), expand4((b >> 20) & 0xF),
-                   expand4((b >> 24) & 0xF), expand4(b >> 28));
-          } else {
-            sts128(a0 + q * 16, oob, oob, oob, oob);
-            sts128(a1 + q * 16, oob, oob, oob, oob);
+            if (p.u8_act) {
+              sts128(a0 + q * 16, spread4(b & 0xF), spread4((b >> 4) & 0xF),
+                     spread4((b >> 8) & 0xF), spread4((b >> 12) & 0xF));
+              sts128(a1 + q * 16, spread4((b >> 16) & 0xF), spread4((b >> 20) & 0xF),
+                     spread4((b >> 24) & 0xF), spread4(b >> 28));
+            } else {
+              sts128(a0 + q * 16, pm4(b & 0xF), pm4((b >> 4) & 0xF), pm4((b >> 8) & 0xF),
+                     pm4((b >> 12) & 0xF));
+              sts128(a1 + q * 16, pm4((b >> 16) & 0xF), pm4((b >> 20) & 0xF),
+                     pm4((b >> 24) & 0xF), pm4(b >> 28));
+            }
+          } else {  // out of bounds: a' = 0, i.e. -1 (u8, neg_one) / a = 0 (s8, zero pad)
+            sts128(a0 + q * 16, 0u, 0u, 0u, 0u);
+            sts128(a1 + q * 16, 0u, 0u, 0u, 0u);
           }
         }
       }
@@ -404,6 +425,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     const int m = quarter * 32 + lane;
     const int groups = p.n_tile / 32;
     const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
+    const int f = p.u8_act ? 2 : 1;
     // bias -> TMEM for every (block, run) unit this warp owns in tile t
     auto init_buffer = [&](int t, int ab) {
       if (t < p.num_tiles) {
@@ -470,38 +492,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
               uint32_t sgn = 0;
 #pragma unroll
               for (int i = 0; i < 32; ++i) sgn |= (v[i] >> 31) << i;
-              w8[rr] = ~sgn;  // bit = acc' >= 0
+              w8[rr] = ~sgn;  // bit = D' >= 0
               if (p.acc && valid) {
                 const int oc = rn.o0 + 32 * rr;
                 const int jc = jt + 32 * gg;
                 int32_t *dst = p.acc + opix * p.c_out + oc;
-                for (int i = 0; i < 32 && oc + i < p.c_out; ++i) {
-                  const int s = __ldg(p.col_sgn + jc + i), bias = __ldg(p.col_bias + jc + i);
-                  dst[i] = s * (int(v[i]) - bias);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  if (oc + i < p.c_out) {
+                    const int s = __ldg(p.col_sgn + jc + i), bias = __ldg(p.col_bias + jc + i);
+                    dst[i] = f * (s * (int(v[i]) - bias)) - __ldg(p.col_w + jc + i);
+                  }
                 }
               }
             }
           }
           if (valid && p.bits) {
-            // write the run; when it ends the pixel's channels append the
-            // zero pad groups of the 128-lane block
+            // write the run; when it ends the pixel's channels append the zero
+            // pad groups of the 128-lane block (w8 is zero past the run)
             uint32_t *dst = p.bits + opix * p.out_stride32 + p.out_off32;
             const int g0 = rn.o0 / 32;
             const int wend = (g0 + rn.len == p.c_out_pad / 32) ? p.out_groups : g0 + rn.len;
-            int gg = g0;
-            while (gg < wend) {
-              const int i = gg - g0;
-              auto wv = [&](int ii) { return ii < rn.len ? w8[ii & 7] : 0u; };
-              if ((gg & 3) == 0 && gg + 4 <= wend) {
-                *reinterpret_cast<uint4 *>(dst + gg) = make_uint4(wv(i), wv(i + 1), wv(i + 2), wv(i + 3));
-                gg += 4;
-              } else if ((gg & 1) == 0 && gg + 2 <= wend) {
-                *reinterpret_cast<uint2 *>(dst + gg) = make_uint2(wv(i), wv(i + 1));
-                gg += 2;
-              } else {
-                dst[gg] = wv(i);
-                gg += 1;
-              }
+            const int cnt = wend - g0;
+            if ((g0 & 3) == 0 && (cnt & 3) == 0 && cnt <= 8) {
+              *reinterpret_cast<uint4 *>(dst + g0) = make_uint4(w8[0], w8[1], w8[2], w8[3]);
+              if (cnt == 8)
+                *reinterpret_cast<uint4 *>(dst + g0 + 4) = make_uint4(w8[4], w8[5], w8[6], w8[7]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (i < cnt) dst[g0 + i] = w8[i];
+              for (int i = 8; i < cnt; ++i) dst[g0 + i] = 0u;
             }
           }
         }
@@ -527,6 +548,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
 // --------------------------------------------------------------------------
 // host side: eligibility, weight repack, launch geometry
 // --------------------------------------------------------------------------
+static int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+static int ceil_div(int a, int b) { return -floor_div(-a, b); }
+
 int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, const int32_t *seg_off,
                     const int32_t *seg_cnt, int n_seg) {
   cv->tc_ok = 0;
@@ -546,7 +570,7 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
     if (any) chunk_word.push_back(c);
   }
   const int kc = int(chunk_word.size());
-  if (kc == 0) return MBU_OK;
+  if (kc == 0 || kc > tc::MAX_CHUNKS) return MBU_OK;
   const int taps = cv->transposed ? 1 : cv->kh * cv->kw;
   const int s2 = cv->transposed ? cv->stride * cv->stride : 1;
   const int c_out_pad = (cv->c_out + 31) / 32 * 32;
@@ -562,11 +586,41 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
   else n_tile = 32;
   const int n_tiles = (n_gemm + n_tile - 1) / n_tile;
   const int n_cols = n_tiles * n_tile;
+  // u8 {0,1} activations are exact when out-of-bounds taps mean -1 (a' = 0);
+  // zero padding needs s8 +-1 / 0.
+  const bool u8 = cv->pad_mode != MBU_PAD_ZERO;
+  const int f = u8 ? 2 : 1;
 
-  // per GEMM column: threshold folded into (weight sign, TMEM bias)
+  // dense s8 weights per (column, tap, chunk lane)
+  const int ptaps = cv->kh * cv->kw;  // taps in the reference plane layout
+  const size_t row_words = size_t(ptaps) * cv->wpp;
+  auto bit = [&](const uint64_t *plane, int o, int tap, int L) -> int {
+    return int((plane[size_t(o) * row_words + size_t(tap) * cv->wpp + (L >> 6)] >> (L & 63)) & 1ull);
+  };
+  auto wval = [&](int j, int tap, int L) -> int {
+    if (j >= n_gemm) return 0;
+    int o = j, ptap = tap;
+    if (cv->transposed) {
+      ptap = j / c_out_pad;
+      o = j % c_out_pad;
+    }
+    if (o >= cv->c_out) return 0;
+    if (neg) return bit(pos, o, ptap, L) - bit(neg, o, ptap, L);
+    return real[L] ? 2 * bit(pos, o, ptap, L) - 1 : 0;
+  };
+  std::vector<int32_t> col_w(size_t(n_cols) + 32, 0);
+  if (u8)
+    for (int j = 0; j < n_gemm; ++j) {
+      int s = 0;
+      for (int tap = 0; tap < taps; ++tap)
+        for (int k = 0; k < kc; ++k)
+          for (int i = 0; i < 32; ++i) s += wval(j, tap, 32 * chunk_word[k] + i);
+      col_w[j] = s;
+    }
+  // per GEMM column: threshold folded into (weight sign, TMEM bias) on D
   std::vector<int32_t> col_bias(size_t(n_cols) + 32, 0), col_sgn(size_t(n_cols) + 32, 1);
   std::vector<int8_t> col_neg(size_t(n_cols), 0);
-  const int kmax = taps * lpp + 1;  // > max |acc|
+  const int dmax = taps * lpp + 1;  // > max |D|
   if (cv->has_threshold) {
     std::vector<int32_t> t(static_cast<size_t>(c_out_pad), 0);
     std::vector<uint8_t> c(static_cast<size_t>(c_out_pad), 2);
@@ -579,46 +633,36 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
         code = c[o];
         T = t[o];
       }
-      // out-of-range thresholds are constants over the reachable accumulators
-      if (code == 0 && T <= -kmax) code = 3;
-      if (code == 0 && T >= kmax) code = 2;
-      if (code == 1 && T >= kmax) code = 3;
-      if (code == 1 && T <= -kmax) code = 2;
+      // acc = f*D - W: GE fires iff D >= ceil((T+W)/f), LE iff D <= floor((T+W)/f)
+      const long long tw = (long long)T + col_w[j];
+      long long dt = 0;
+      if (code == 0) dt = (tw >= 2LL * dmax * f) ? (long long)dmax : (tw <= -2LL * dmax * f) ? -(long long)dmax : ceil_div(int(tw), f);
+      if (code == 1) dt = (tw >= 2LL * dmax * f) ? (long long)dmax : (tw <= -2LL * dmax * f) ? -(long long)dmax : floor_div(int(tw), f);
+      // out-of-range decision points are constants over the reachable D
+      if (code == 0 && dt <= -dmax) code = 3;
+      if (code == 0 && dt >= dmax) code = 2;
+      if (code == 1 && dt >= dmax) code = 3;
+      if (code == 1 && dt <= -dmax) code = 2;
       switch (code) {
-        case 0: col_bias[j] = -T; col_sgn[j] = 1; break;                 // acc - T >= 0
-        case 1: col_bias[j] = T; col_sgn[j] = -1; col_neg[j] = 1; break;  // T - acc >= 0
-        case 3: col_bias[j] = kmax; col_sgn[j] = 1; break;               // always >= 0
-        default: col_bias[j] = -2 * kmax; col_sgn[j] = 1; break;         // always < 0
+        case 0: col_bias[j] = int(-dt); col_sgn[j] = 1; break;                 // D - D_T >= 0
+        case 1: col_bias[j] = int(dt); col_sgn[j] = -1; col_neg[j] = 1; break;  // D_T - D >= 0
+        case 3: col_bias[j] = dmax; col_sgn[j] = 1; break;                     // always >= 0
+        default: col_bias[j] = -2 * dmax; col_sgn[j] = 1; break;               // always < 0
       }
     }
   }
   const size_t b_stage = size_t(taps) * n_tile * 32;
   std::vector<int8_t> b(size_t(n_tiles) * kc * b_stage, 0);
-  const int ptaps = cv->kh * cv->kw;  // taps in the reference plane layout
-  const size_t row_words = size_t(ptaps) * cv->wpp;
-  auto bit = [&](const uint64_t *plane, int o, int tap, int L) -> int {
-    return int((plane[size_t(o) * row_words + size_t(tap) * cv->wpp + (L >> 6)] >> (L & 63)) & 1ull);
-  };
   for (int nt = 0; nt < n_tiles; ++nt)
     for (int k = 0; k < kc; ++k)
       for (int tap = 0; tap < taps; ++tap)
         for (int half = 0; half < 2; ++half)
           for (int n = 0; n < n_tile; ++n) {
             const int j = nt * n_tile + n;
-            if (j >= n_gemm) continue;
-            int o = j, ptap = tap;
-            if (cv->transposed) {
-              ptap = j / c_out_pad;
-              o = j % c_out_pad;
-            }
-            if (o >= cv->c_out) continue;
             int8_t *dst = &b[((size_t(nt) * kc + k) * taps + tap) * n_tile * 32 + size_t(half) * n_tile * 16 +
                              size_t(n) * 16];
             for (int i = 0; i < 16; ++i) {
-              const int L = 32 * chunk_word[k] + 16 * half + i;
-              int v;
-              if (neg) v = bit(pos, o, ptap, L) - bit(neg, o, ptap, L);
-              else v = real[L] ? 2 * bit(pos, o, ptap, L) - 1 : 0;
+              const int v = wval(j, tap, 32 * chunk_word[k] + 16 * half + i);
               dst[i] = int8_t(col_neg[j] ? -v : v);
             }
           }
@@ -630,6 +674,7 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
                      "upload chunk map"));
   std::vector<int32_t> cols(col_bias);
   cols.insert(cols.end(), col_sgn.begin(), col_sgn.end());
+  cols.insert(cols.end(), col_w.begin(), col_w.end());
   MBU_TRY(check_cuda(cudaMalloc(&cv->d_thr2, cols.size() * sizeof(int32_t)), "alloc column bias"));
   MBU_TRY(check_cuda(cudaMemcpy(cv->d_thr2, cols.data(), cols.size() * sizeof(int32_t), cudaMemcpyHostToDevice),
                      "upload column bias"));
@@ -678,6 +723,9 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   p.w = x.w;
   p.x_stride32 = x.stride * 2;
   p.x_off32 = x.offset * 2;
+  // producers index the input with 32-bit word offsets
+  if ((int64_t(x.n) * x.h * x.w + 2 * int64_t(x.w) + 4) * p.x_stride32 >= (int64_t(1) << 31))
+    return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv input larger than 2^31 words");
   p.halo = cv->taps == 9 ? 1 : 0;
   p.n_tile = cv->n_tile;
   p.n_tiles = cv->n_tiles;
@@ -712,13 +760,14 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   int stages = int((227 * 1024 - tc::SMEM_HEADER) / stage);
   if (stages < 2) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv stage does not fit in shared memory");
   p.stages = std::min(stages, tc::MAX_STAGES);
-  p.zero_pad = cv->pad_mode == MBU_PAD_ZERO;
+  p.u8_act = cv->pad_mode != MBU_PAD_ZERO;
   p.kc = cv->kc;
   p.chunk_word = cv->d_chunk_word;
   p.b = cv->d_b;
-  // instruction descriptor: s32 accum, s8 x s8, K-major both, N, M = 128
-  p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(cv->n_tile >> 3) << 17) |
-            (uint32_t(tc::BLOCK_M >> 4) << 24);
+  // instruction descriptor: s32 accum, A u8 (neg_one) / s8 (zero pad), B s8,
+  // K-major both, N, M = 128
+  p.idesc = (2u << 4) | (uint32_t(p.u8_act ? 0 : 1) << 7) | (1u << 10) |
+            (uint32_t(cv->n_tile >> 3) << 17) | (uint32_t(tc::BLOCK_M >> 4) << 24);
   p.c_out = cv->c_out;
   p.c_out_pad = cv->c_out_pad;
   p.n_gemm = cv->n_gemm;
@@ -732,6 +781,7 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   p.out_groups = cv->out_wpp * 2;
   p.col_bias = static_cast<const int32_t *>(cv->d_thr2);
   p.col_sgn = p.col_bias + cv->n_pad + 32;
+  p.col_w = p.col_sgn + cv->n_pad + 32;
   const int64_t tiles = int64_t(x.n) * p.row_tiles * p.col_tiles * p.n_tiles;
   if (tiles == 0) return MBU_OK;
   if (tiles > 0x7FFFFFFF) return fail(MBU_ERR_SHAPE, "tcgen05 conv grid too large");
