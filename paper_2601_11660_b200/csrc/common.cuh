@@ -106,7 +106,8 @@ struct mbu_fconv {
   double *d_bn = nullptr;     // gamma, beta, mean, sigma (4*c_out)
   int32_t *d_lanes = nullptr; // input lane per channel (bits input)
   int stem_fast = 0;          // float32 + exact-recheck stem kernel usable
-  void *d_stem = nullptr;     // StemConsts (endpoints.cu)
+  void *d_stem = nullptr;     // unused (kept for ABI of the struct)
+  void *h_stem = nullptr;     // StemConsts host copy, passed as a kernel parameter
   int head_tab = 0;           // byte-table head usable (contiguous input lanes from 0)
   double *d_head_tab = nullptr;  // [c_out][ceil(c_in/8)][256] signed partial sums
 };
@@ -132,4 +133,5 @@ int launch_stem_fast(const mbu_fconv *fc, const double *x, int n, int h, int w, 
 int launch_head_fast(const mbu_fconv *fc, const ActView &xb, int n, int h, int w, double *logits,
                      uint8_t *mask, cudaStream_t st);
 int head_prepare(mbu_fconv *fc, const double *w, const int32_t *lanes);
+void stem_free(mbu_fconv *fc);
 }  // namespace mbu

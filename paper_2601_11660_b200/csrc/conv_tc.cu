@@ -72,6 +72,8 @@ constexpr int MAX_CHUNKS = 64;  // 32-lane chunks per pixel (2048 lanes)
 constexpr int SMEM_HEADER = 1024;
 constexpr int MIN_SMEM = 120 * 1024;  // > half an SM: exactly one CTA (and TMEM owner) per SM
 constexpr int PROD_ITEMS = 6;         // strip rows per producer thread per stage (Q <= 6*256)
+constexpr int LOOKAHEAD = 4;          // raw-bit stages in flight per producer thread
+constexpr int RAW_STAGES = LOOKAHEAD + 1;
 
 struct Params {
   const uint32_t *x32;
@@ -290,46 +292,70 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     // Per tile, each thread caches the 32-bit word offset of its strip rows
     // (and an in-bounds mask); per stage it only adds the chunk's word index.
     // The loads of stage g+1 are issued before stage g is expanded.
+    // Raw words travel global -> smem with cp.async (zero-filled when out of
+    // bounds) LOOKAHEAD stages ahead of the expansion, so DRAM latency is
+    // overlapped with the expansion and MMAs of earlier stages. Each thread
+    // expands exactly the rows it copied, so cp.async.wait_group is the only
+    // synchronisation needed. Per tile, each thread caches the 32-bit word
+    // offsets of its strip rows and an in-bounds mask.
     const int pt = threadIdx.x - PROD_WARP0 * 32;
     const int strip_rows = p.R + 2 * p.halo;
-    int off[PROD_ITEMS];
-    uint32_t inb = 0;
-    int cached_t = -1;
-    auto tile_offsets = [&](int t) {
+    uint32_t *raw = reinterpret_cast<uint32_t *>(b_base + size_t(p.stages) * p.b_stage_bytes);
+    struct Cache {
+      int t = -1;
+      int off[PROD_ITEMS];
+      uint32_t inb = 0;
+    };
+    Cache ic, ec;  // issue-side and expand-side tile caches
+    auto tile_offsets = [&](Cache &c, int t) {
       const Tile tl = decode_tile(p, t);
-      inb = 0;
+      c.inb = 0;
 #pragma unroll
       for (int j = 0; j < PROD_ITEMS; ++j) {
         const int q = pt + j * PROD_THREADS;
         const int rr = int(__umulhi(uint32_t(q), p.p_magic));
         const int iy = tl.y0 - p.halo + rr;
         const int ix = tl.x0 - p.halo + (q - rr * p.P);
-        off[j] = ((tl.nb * p.h + iy) * p.w + ix) * p.x_stride32 + p.x_off32;
-        if (q < p.Q && rr < strip_rows && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w) inb |= 1u << j;
+        c.off[j] = ((tl.nb * p.h + iy) * p.w + ix) * p.x_stride32 + p.x_off32;
+        if (q < p.Q && rr < strip_rows && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w) c.inb |= 1u << j;
       }
-      cached_t = t;
+      c.t = t;
     };
-    uint32_t cur[PROD_ITEMS], nxt[PROD_ITEMS];
-    uint32_t inb_cur = 0, inb_nxt = 0;
-    auto load_stage = [&](int t, int k, uint32_t (&wd)[PROD_ITEMS]) -> uint32_t {
-      if (t != cached_t) tile_offsets(t);
-      const int cw = chunk_s[k];
+    // stage g <-> (tile blockIdx.x + (g / kc) * gridDim.x, chunk g % kc)
+    const int tiles_here = p.num_tiles > int(blockIdx.x)
+                               ? (p.num_tiles - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x)
+                               : 0;
+    const int n_stages_total = tiles_here * p.kc;
+    auto issue = [&](int g) {
+      if (g < n_stages_total) {
+        const int t = blockIdx.x + (g / p.kc) * gridDim.x;
+        if (t != ic.t) tile_offsets(ic, t);
+        const int cw = chunk_s[g % p.kc];
+        uint32_t *dst = raw + (g % RAW_STAGES) * p.Q;
 #pragma unroll
-      for (int j = 0; j < PROD_ITEMS; ++j) wd[j] = ((inb >> j) & 1) ? __ldg(p.x32 + off[j] + cw) : 0u;
-      return inb;
-    };
-    int t = blockIdx.x, k = 0;
-    if (t < p.num_tiles) inb_cur = load_stage(t, 0, cur);
-    int k_global = 0;
-    while (t < p.num_tiles) {
-      int tn = t, kn = k + 1;
-      if (kn == p.kc) {
-        kn = 0;
-        tn += gridDim.x;
+        for (int j = 0; j < PROD_ITEMS; ++j) {
+          const int q = pt + j * PROD_THREADS;
+          if (q < p.Q) {
+            const bool in = (ic.inb >> j) & 1;
+            const uint32_t *src = p.x32 + (in ? ic.off[j] + cw : 0);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst + q)),
+                         "l"(src), "r"(in ? 4 : 0)
+                         : "memory");
+          }
+        }
       }
-      if (tn < p.num_tiles) inb_nxt = load_stage(tn, kn, nxt);
-      const int s = k_global % S;
-      const int u = k_global / S;
+      asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group g
+    };
+#pragma unroll 1
+    for (int g = 0; g < LOOKAHEAD; ++g) issue(g);
+    for (int g = 0; g < n_stages_total; ++g) {
+      issue(g + LOOKAHEAD);
+      asm volatile("cp.async.wait_group %0;" ::"n"(LOOKAHEAD) : "memory");  // group g landed
+      const int t = blockIdx.x + (g / p.kc) * gridDim.x;
+      if (t != ec.t) tile_offsets(ec, t);
+      const uint32_t *rw = raw + (g % RAW_STAGES) * p.Q;
+      const int s = g % S;
+      const int u = g / S;
       if (u > 0) mbar_wait(smem_u32(&empty[s]), (u - 1) & 1);
       const uint32_t a0 = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
       const uint32_t a1 = a0 + p.Q * 16;
@@ -337,8 +363,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       for (int j = 0; j < PROD_ITEMS; ++j) {
         const int q = pt + j * PROD_THREADS;
         if (q < p.Q) {
-          const uint32_t b = cur[j];
-          if ((inb_cur >> j) & 1) {
+          const uint32_t b = rw[q];
+          if ((ec.inb >> j) & 1) {
             if (p.u8_act) {
               sts128(a0 + q * 16, spread4(b & 0xF), spread4((b >> 4) & 0xF),
                      spread4((b >> 8) & 0xF), spread4((b >> 12) & 0xF));
@@ -358,13 +384,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       }
       fence_proxy_async();
       mbar_arrive(smem_u32(&full[s]));
-#pragma unroll
-      for (int j = 0; j < PROD_ITEMS; ++j) cur[j] = nxt[j];
-      inb_cur = inb_nxt;
-      t = tn;
-      k = kn;
-      ++k_global;
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
   } else if (warp == MMA_WARP) {
     // ============ single-thread MMA issue (accumulators pre-loaded with bias) ============
     if (lane == 0) {
@@ -757,7 +778,8 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   p.a_stage_bytes = uint32_t((size_t(Q) * 32 + 1023) / 1024 * 1024);
   p.b_stage_bytes = uint32_t(cv->b_stage_bytes);
   const size_t stage = size_t(p.a_stage_bytes) + p.b_stage_bytes;
-  int stages = int((227 * 1024 - tc::SMEM_HEADER) / stage);
+  const size_t raw_bytes = size_t(tc::RAW_STAGES) * Q * 4;
+  int stages = int((227 * 1024 - tc::SMEM_HEADER - raw_bytes) / stage);
   if (stages < 2) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv stage does not fit in shared memory");
   p.stages = std::min(stages, tc::MAX_STAGES);
   p.u8_act = cv->pad_mode != MBU_PAD_ZERO;
@@ -787,7 +809,7 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   if (tiles > 0x7FFFFFFF) return fail(MBU_ERR_SHAPE, "tcgen05 conv grid too large");
   p.num_tiles = int(tiles);
   const int grid = int(std::min<int64_t>(tiles, num_sms()));
-  size_t smem = tc::SMEM_HEADER + size_t(p.stages) * stage;
+  size_t smem = tc::SMEM_HEADER + size_t(p.stages) * stage + raw_bytes;
   smem = std::max<size_t>(smem, tc::MIN_SMEM);
   if (cv->transposed) return launch_tc_impl<1, true>(p, grid, smem, st);
   if (cv->taps == 9) return launch_tc_impl<9, false>(p, grid, smem, st);

@@ -56,14 +56,13 @@ template <int CIN>
 __global__ void __launch_bounds__(STEM_TX *STEM_TY) stem_kernel(
     const double *__restrict__ x, int n, int h, int w, int c_out,
     const double *__restrict__ w64, const double *__restrict__ bias64,
-    const double *__restrict__ bn, const StemConsts *__restrict__ k,
+    const double *__restrict__ bn, const __grid_constant__ StemConsts ks,
     uint32_t *__restrict__ bits, int out_stride32, int out_offset32, int out_groups) {
+  // the float32 weights and per-channel constants live in the kernel
+  // parameter bank: FFMA2 reads them as constant operands, no shared memory
   __shared__ double tile[STEM_TY + 2][STEM_TX + 2][CIN];
-  __shared__ __align__(16) StemConsts ks;
   const int tx = threadIdx.x % STEM_TX, ty = threadIdx.x / STEM_TX;
   const int x0 = blockIdx.x * STEM_TX, y0 = blockIdx.y * STEM_TY, nb = blockIdx.z;
-  for (int i = threadIdx.x; i < int(sizeof(StemConsts) / 16); i += blockDim.x)
-    reinterpret_cast<uint4 *>(&ks)[i] = reinterpret_cast<const uint4 *>(k)[i];
   for (int i = threadIdx.x; i < (STEM_TY + 2) * (STEM_TX + 2); i += blockDim.x) {
     const int r = i / (STEM_TX + 2), c = i % (STEM_TX + 2);
     const int iy = y0 - 1 + r, ix = x0 - 1 + c;
@@ -89,13 +88,9 @@ __global__ void __launch_bounds__(STEM_TX *STEM_TY) stem_kernel(
       finite &= isfinite(d);
       const float xf = float(d);
       xmax = fmaxf(xmax, fabsf(xf));
-      const uint4 *wr = reinterpret_cast<const uint4 *>(ks.w[t * CIN + ci]);
+      const unsigned long long *wr = reinterpret_cast<const unsigned long long *>(ks.w[t * CIN + ci]);
 #pragma unroll
-      for (int q = 0; q < STEM_COUT / 4; ++q) {
-        const uint4 wv = wr[q];
-        acc[2 * q] = ffma2_bcast(xf, (unsigned long long)wv.x | ((unsigned long long)wv.y << 32), acc[2 * q]);
-        acc[2 * q + 1] = ffma2_bcast(xf, (unsigned long long)wv.z | ((unsigned long long)wv.w << 32), acc[2 * q + 1]);
-      }
+      for (int q = 0; q < STEM_COUT / 2; ++q) acc[q] = ffma2_bcast(xf, wr[q], acc[q]);
     }
   }
   uint32_t word[2] = {0u, 0u};
@@ -184,18 +179,21 @@ int stem_prepare(mbu_fconv *fc, const double *w, const double *bias, const doubl
       }
     }
   }
-  MBU_TRY(check_cuda(cudaMalloc(&fc->d_stem, sizeof(StemConsts)), "alloc stem consts"));
-  MBU_TRY(check_cuda(cudaMemcpy(fc->d_stem, &k, sizeof(StemConsts), cudaMemcpyHostToDevice),
-                     "upload stem consts"));
+  fc->h_stem = new StemConsts(k);  // passed by value as a __grid_constant__ kernel parameter
   fc->stem_fast = 1;
   return MBU_OK;
+}
+
+void stem_free(mbu_fconv *fc) {
+  delete static_cast<StemConsts *>(fc->h_stem);
+  fc->h_stem = nullptr;
 }
 
 int launch_stem_fast(const mbu_fconv *fc, const double *x, int n, int h, int w, uint64_t *bits,
                      int out_stride, int out_offset, cudaStream_t st) {
   dim3 grid((w + STEM_TX - 1) / STEM_TX, (h + STEM_TY - 1) / STEM_TY, n);
   const int groups = ((fc->c_out + 127) / 128) * 4;
-  auto *k = static_cast<const StemConsts *>(fc->d_stem);
+  const StemConsts &k = *static_cast<const StemConsts *>(fc->h_stem);
   auto *b32 = reinterpret_cast<uint32_t *>(bits);
 #define MBU_STEM(C)                                                                          \
   stem_kernel<C><<<grid, STEM_TX * STEM_TY, 0, st>>>(x, n, h, w, fc->c_out, fc->d_w, fc->d_bias, \

@@ -552,7 +552,7 @@ int mbu_fconv_destroy(mbu_fconv *fc) {
   cudaFree(fc->d_bias);
   cudaFree(fc->d_bn);
   cudaFree(fc->d_lanes);
-  cudaFree(fc->d_stem);
+  stem_free(fc);
   cudaFree(fc->d_head_tab);
   delete fc;
   return MBU_OK;
