@@ -115,14 +115,17 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
 }
+// try_wait with a suspend-time hint: the waiting thread is parked by the
+// hardware until the phase flips (or ~10 ms), instead of re-issuing the wait
+// and stealing issue slots from the producer / epilogue warps.
 __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(bar), "r"(parity)
+      : "r"(bar), "r"(parity), "r"(0x989680)
       : "memory");
   return ok != 0;
 }
@@ -275,6 +278,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = threadIdx.x; i < p.kc; i += blockDim.x) chunk_s[i] = p.chunk_word[i];
+  // per-N-tile epilogue runs and per-column TMEM biases, staged once per CTA
+  int4 *runs_s = reinterpret_cast<int4 *>(b_base + size_t(p.stages) * p.b_stage_bytes +
+                                          size_t(RAW_STAGES) * p.Q * 4);
+  int32_t *bias_s = reinterpret_cast<int32_t *>(runs_s + p.n_tiles * 8);
+  for (int i = threadIdx.x; i < p.n_tiles * p.n_tile; i += blockDim.x) bias_s[i] = p.col_bias[i];
+  if (threadIdx.x < p.n_tiles) {
+    const int nt = threadIdx.x, groups = p.n_tile / 32;
+    int g = 0, r = 0;
+    while (g < groups && r < 8) {
+      const Run rn = run_at(p, nt * p.n_tile, g, groups, TCONV);
+      if (rn.len == 0) break;
+      runs_s[nt * 8 + r++] = make_int4(rn.g, rn.len, rn.o0, rn.tap);
+      g += rn.len;
+    }
+    for (; r < 8; ++r) runs_s[nt * 8 + r] = make_int4(0, 0, 0, 0);
+  }
   if (warp == MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
@@ -444,25 +463,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     const int quarter = warp & 3;
     const int half = warp >> 2;
     const int m = quarter * 32 + lane;
-    const int groups = p.n_tile / 32;
     const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
     const int f = p.u8_act ? 2 : 1;
+    // unit (block b, run ri) belongs to this warp iff its parity matches
+    auto mine = [&](int b, int ri) { return ((p.MB >= 2 ? b : ri) & 1) == half; };
     // bias -> TMEM for every (block, run) unit this warp owns in tile t
     auto init_buffer = [&](int t, int ab) {
       if (t < p.num_tiles) {
-        const int jt = (t % p.n_tiles) * p.n_tile;
-        int ri = 0;
-        for (int g = 0; g < groups; ++ri) {
-          const Run rn = run_at(p, jt, g, groups, TCONV);
-          if (rn.len == 0) break;
+        const int nt = t % p.n_tiles;
+        const int jt = nt * p.n_tile;
+        for (int ri = 0; ri < 8; ++ri) {
+          const int4 rn = runs_s[nt * 8 + ri];
+          if (rn.y == 0) break;
           for (int b = 0; b < p.MB; ++b) {
-            if ((p.MB >= 2 ? b : ri) % 2 != half) continue;
-            for (int gg = rn.g; gg < rn.g + rn.len; ++gg) {
+            if (!mine(b, ri)) continue;
+            for (int gg = rn.x; gg < rn.x + rn.y; ++gg) {
               uint32_t v[32];
-              const int4 *src = reinterpret_cast<const int4 *>(p.col_bias + jt + 32 * gg);
+              const int4 *src = reinterpret_cast<const int4 *>(bias_s + jt + 32 * gg);
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                const int4 q4 = __ldg(src + i);
+                const int4 q4 = src[i];
                 v[4 * i] = q4.x;
                 v[4 * i + 1] = q4.y;
                 v[4 * i + 2] = q4.z;
@@ -471,7 +491,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
               tmem_st32(lane_base + uint32_t(ab * ACC_COLS + b * p.n_tile + gg * 32), v);
             }
           }
-          g += rn.len;
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
@@ -487,41 +506,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       mbar_wait(smem_u32(&acc_full[ab]), (it >> 1) & 1);
       tc_fence_after();
       const int jt = tl.nt * p.n_tile;
-      int ri = 0;
-      for (int g = 0; g < groups; ++ri) {
-        const Run rn = run_at(p, jt, g, groups, TCONV);
-        if (rn.len == 0) break;
+      for (int ri = 0; ri < 8; ++ri) {
+        const int4 rn = runs_s[tl.nt * 8 + ri];  // (first group, length, o0, tap)
+        if (rn.y == 0) break;
         for (int b = 0; b < p.MB; ++b) {
-          if ((p.MB >= 2 ? b : ri) % 2 != half) continue;
+          if (!mine(b, ri)) continue;
           const int q = block_q0(p, b) + m;
           const int rq = int(__umulhi(uint32_t(q), p.p_magic));
           const int r = rq - p.halo;
           const int c = q - rq * p.P - p.halo;
           const int yy = tl.y0 + r, xx = tl.x0 + c;
           const bool valid = r >= 0 && r < p.R && c >= 0 && c < p.TW && yy < p.h && xx < p.w;
-          const int oy = TCONV ? yy * p.tconv_s + rn.tap / p.tconv_s : yy;
-          const int ox = TCONV ? xx * p.tconv_s + rn.tap % p.tconv_s : xx;
+          int oy = yy, ox = xx;
+          if (TCONV) {
+            const int dy = rn.w / p.tconv_s;
+            oy = yy * p.tconv_s + dy;
+            ox = xx * p.tconv_s + (rn.w - dy * p.tconv_s);
+          }
           const int64_t opix = (int64_t(tl.nb) * p.ho + oy) * p.wo + ox;
           uint32_t w8[8];
 #pragma unroll
           for (int rr = 0; rr < 8; ++rr) {
             w8[rr] = 0u;
-            if (rr < rn.len) {
+            if (rr < rn.y) {
               uint32_t v[32];
-              const int gg = rn.g + rr;
+              const int gg = rn.x + rr;
               tmem_ld32(lane_base + uint32_t(ab * ACC_COLS + b * p.n_tile + gg * 32), v);
               uint32_t sgn = 0;
 #pragma unroll
               for (int i = 0; i < 32; ++i) sgn |= (v[i] >> 31) << i;
               w8[rr] = ~sgn;  // bit = D' >= 0
               if (p.acc && valid) {
-                const int oc = rn.o0 + 32 * rr;
+                const int oc = rn.z + 32 * rr;
                 const int jc = jt + 32 * gg;
                 int32_t *dst = p.acc + opix * p.c_out + oc;
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                   if (oc + i < p.c_out) {
-                    const int s = __ldg(p.col_sgn + jc + i), bias = __ldg(p.col_bias + jc + i);
+                    const int s = __ldg(p.col_sgn + jc + i), bias = bias_s[jc + i];
                     dst[i] = f * (s * (int(v[i]) - bias)) - __ldg(p.col_w + jc + i);
                   }
                 }
@@ -532,8 +554,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             // write the run; when it ends the pixel's channels append the zero
             // pad groups of the 128-lane block (w8 is zero past the run)
             uint32_t *dst = p.bits + opix * p.out_stride32 + p.out_off32;
-            const int g0 = rn.o0 / 32;
-            const int wend = (g0 + rn.len == p.c_out_pad / 32) ? p.out_groups : g0 + rn.len;
+            const int g0 = rn.z >> 5;
+            const int wend = (g0 + rn.y == p.c_out_pad / 32) ? p.out_groups : g0 + rn.y;
             const int cnt = wend - g0;
             if ((g0 & 3) == 0 && (cnt & 3) == 0 && cnt <= 8) {
               *reinterpret_cast<uint4 *>(dst + g0) = make_uint4(w8[0], w8[1], w8[2], w8[3]);
@@ -547,7 +569,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             }
           }
         }
-        g += rn.len;
       }
       // buffer drained: re-arm it with the bias of the tile that reuses it
       init_buffer(t + 2 * gridDim.x, ab);
@@ -778,7 +799,9 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   p.a_stage_bytes = uint32_t((size_t(Q) * 32 + 1023) / 1024 * 1024);
   p.b_stage_bytes = uint32_t(cv->b_stage_bytes);
   const size_t stage = size_t(p.a_stage_bytes) + p.b_stage_bytes;
-  const size_t raw_bytes = size_t(tc::RAW_STAGES) * Q * 4;
+  // raw-bit ring + per-N-tile run table + per-column biases
+  const size_t raw_bytes = size_t(tc::RAW_STAGES) * Q * 4 + size_t(cv->n_tiles) * 8 * 16 +
+                           size_t(cv->n_tiles) * cv->n_tile * 4;
   int stages = int((227 * 1024 - tc::SMEM_HEADER - raw_bytes) / stage);
   if (stages < 2) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv stage does not fit in shared memory");
   p.stages = std::min(stages, tc::MAX_STAGES);
