@@ -289,7 +289,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     while (g < groups && r < 8) {
       const Run rn = run_at(p, nt * p.n_tile, g, groups, TCONV);
       if (rn.len == 0) break;
-      runs_s[nt * 8 + r++] = make_int4(rn.g, rn.len, rn.o0, rn.tap);
+      const int dy = TCONV ? rn.tap / p.tconv_s : 0;
+      runs_s[nt * 8 + r++] = make_int4(rn.g, rn.len, rn.o0, (dy << 16) | (rn.tap - dy * p.tconv_s));
       g += rn.len;
     }
     for (; r < 8; ++r) runs_s[nt * 8 + r] = make_int4(0, 0, 0, 0);
@@ -345,12 +346,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
                                ? (p.num_tiles - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x)
                                : 0;
     const int n_stages_total = tiles_here * p.kc;
-    auto issue = [&](int g) {
-      if (g < n_stages_total) {
-        const int t = blockIdx.x + (g / p.kc) * gridDim.x;
-        if (t != ic.t) tile_offsets(ic, t);
-        const int cw = chunk_s[g % p.kc];
-        uint32_t *dst = raw + (g % RAW_STAGES) * p.Q;
+    // incremental cursors (no integer division in the per-stage loop)
+    int i_t = blockIdx.x, i_k = 0, i_slot = 0, i_g = 0;        // issue side
+    int e_t = blockIdx.x, e_k = 0, e_slot = 0, s = 0, ph = 0;  // expand side
+    auto issue = [&]() {
+      if (i_g < n_stages_total) {
+        if (i_t != ic.t) tile_offsets(ic, i_t);
+        const int cw = chunk_s[i_k];
+        uint32_t *dst = raw + i_slot * p.Q;
 #pragma unroll
         for (int j = 0; j < PROD_ITEMS; ++j) {
           const int q = pt + j * PROD_THREADS;
@@ -363,19 +366,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           }
         }
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group g
+      asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group
+      ++i_g;
+      if (++i_k == p.kc) {
+        i_k = 0;
+        i_t += gridDim.x;
+      }
+      if (++i_slot == RAW_STAGES) i_slot = 0;
     };
 #pragma unroll 1
-    for (int g = 0; g < LOOKAHEAD; ++g) issue(g);
+    for (int g = 0; g < LOOKAHEAD; ++g) issue();
     for (int g = 0; g < n_stages_total; ++g) {
-      issue(g + LOOKAHEAD);
+      issue();
       asm volatile("cp.async.wait_group %0;" ::"n"(LOOKAHEAD) : "memory");  // group g landed
-      const int t = blockIdx.x + (g / p.kc) * gridDim.x;
-      if (t != ec.t) tile_offsets(ec, t);
-      const uint32_t *rw = raw + (g % RAW_STAGES) * p.Q;
-      const int s = g % S;
-      const int u = g / S;
-      if (u > 0) mbar_wait(smem_u32(&empty[s]), (u - 1) & 1);
+      if (e_t != ec.t) tile_offsets(ec, e_t);
+      const uint32_t *rw = raw + e_slot * p.Q;
+      if (g >= S) mbar_wait(smem_u32(&empty[s]), ph ^ 1);
       const uint32_t a0 = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
       const uint32_t a1 = a0 + p.Q * 16;
 #pragma unroll
@@ -403,6 +409,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       }
       fence_proxy_async();
       mbar_arrive(smem_u32(&full[s]));
+      if (++e_k == p.kc) {
+        e_k = 0;
+        e_t += gridDim.x;
+      }
+      if (++e_slot == RAW_STAGES) e_slot = 0;
+      if (++s == S) {
+        s = 0;
+        ph ^= 1;
+      }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
   } else if (warp == MMA_WARP) {
@@ -411,15 +426,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       const uint32_t sbo = 128;
       const uint32_t a_lbo = uint32_t(p.Q) * 16;
       const uint32_t b_lbo = uint32_t(p.n_tile) * 16;
-      int k_global = 0, it = 0;
+      int s = 0, ph = 0, it = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         const int ab = it & 1;
         mbar_wait(smem_u32(&acc_empty[ab]), (it >> 1) & 1);
         tc_fence_after();
         const uint32_t d0 = tmem + uint32_t(ab * ACC_COLS);
-        for (int k = 0; k < p.kc; ++k, ++k_global) {
-          const int s = k_global % S;
-          mbar_wait(smem_u32(&full[s]), (k_global / S) & 1);
+        for (int k = 0; k < p.kc; ++k) {
+          mbar_wait(smem_u32(&full[s]), ph);
           tc_fence_after();
           const uint32_t a_s = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
           const uint32_t b_s = smem_u32(b_base + size_t(s) * p.b_stage_bytes);
@@ -434,6 +448,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             }
           }
           umma_commit(smem_u32(&empty[s]));
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
         }
         umma_commit(smem_u32(&acc_full[ab]));
       }
@@ -442,18 +460,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
   } else if (warp == BLOAD_WARP) {
     // ============ weight stages: one bulk copy per stage ============
     if (lane == 0) {
-      int k_global = 0;
+      int s = 0, ph = 0, g = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
         const int nt = t % p.n_tiles;
         const int8_t *src = p.b + size_t(nt) * p.kc * p.b_stage_bytes;
-        for (int k = 0; k < p.kc; ++k, ++k_global) {
-          const int s = k_global % S;
-          const int u = k_global / S;
-          if (u > 0) mbar_wait(smem_u32(&empty[s]), (u - 1) & 1);
+        for (int k = 0; k < p.kc; ++k, ++g) {
+          if (g >= S) mbar_wait(smem_u32(&empty[s]), ph ^ 1);
           const uint32_t bar = smem_u32(&full[s]);
           mbar_arrive_expect_tx(bar, p.b_stage_bytes);
           bulk_g2s(smem_u32(b_base + size_t(s) * p.b_stage_bytes),
                    src + size_t(k) * p.b_stage_bytes, p.b_stage_bytes, bar);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
         }
       }
     }
@@ -518,10 +538,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           const int yy = tl.y0 + r, xx = tl.x0 + c;
           const bool valid = r >= 0 && r < p.R && c >= 0 && c < p.TW && yy < p.h && xx < p.w;
           int oy = yy, ox = xx;
-          if (TCONV) {
-            const int dy = rn.w / p.tconv_s;
-            oy = yy * p.tconv_s + dy;
-            ox = xx * p.tconv_s + (rn.w - dy * p.tconv_s);
+          if (TCONV) {  // run's tap = (dy, dx) packed as dy << 16 | dx
+            oy = yy * p.tconv_s + (rn.w >> 16);
+            ox = xx * p.tconv_s + (rn.w & 0xFFFF);
           }
           const int64_t opix = (int64_t(tl.nb) * p.ho + oy) * p.wo + ox;
           uint32_t w8[8];
