@@ -159,18 +159,61 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   d |= uint64_t(1) << 46;
   return d;
 }
-__device__ __forceinline__ void umma_i8_acc(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc) {
+// The MMA warp runs converged; elect.sync inside the asm picks the issuing
+// lane, so ptxas emits bare UTCIMMAs on uniform registers instead of an
+// ELECT/BRA.U.ANY loop around every MMA (the per-MMA issue cost is what
+// bounds the N = 64 layers, whose MMAs take only 32 tensor cycles).
+// Nine taps of one M block: A = the strip descriptor of the centre tap moved
+// by (dy-1)*P + (dx-1) rows of 16 B, B = one weight slab per tap.
+__device__ __forceinline__ void umma9_i8(uint32_t tmem_d, uint64_t a_c, uint64_t b0, uint64_t pp,
+                                         uint64_t bs, uint32_t idesc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 am, ap, a, b;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
       "setp.ne.b32 p, 1, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "sub.s64 am, %1, %3;\n\t"
+      "add.s64 ap, %1, %3;\n\t"
+      "add.s64 a, am, -1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a, %2, %5, p;\n\t"
+      "add.s64 b, %2, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], am, b, %5, p;\n\t"
+      "add.s64 a, am, 1;\n\t"
+      "add.s64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a, b, %5, p;\n\t"
+      "add.s64 a, %1, -1;\n\t"
+      "add.s64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a, b, %5, p;\n\t"
+      "add.s64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, b, %5, p;\n\t"
+      "add.s64 a, %1, 1;\n\t"
+      "add.s64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a, b, %5, p;\n\t"
+      "add.s64 a, ap, -1;\n\t"
+      "add.s64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a, b, %5, p;\n\t"
+      "add.s64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], ap, b, %5, p;\n\t"
+      "add.s64 a, ap, 1;\n\t"
+      "add.s64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a, b, %5, p;\n\t}" ::"r"(tmem_d),
+      "l"(a_c), "l"(b0), "l"(pp), "l"(bs), "r"(idesc)
+      : "memory");
+}
+__device__ __forceinline__ void umma1_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, 1, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc)
       : "memory");
 }
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   bar)
-               : "memory");
+__device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+      : "memory");
 }
 #define MBU_R32(v)                                                                             \
   "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),      \
@@ -190,6 +233,41 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// 64 consecutive accumulator columns of this thread's TMEM lane, one wait
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&v)[64]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+      "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+      "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]),
+        "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]),
+        "=r"(v[38]), "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]),
+        "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]),
+        "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]),
+        "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]),
+        "=r"(v[62]), "=r"(v[63])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// bit i = NOT sign(v[OFF + i]), i.e. (D' >= 0): four independent funnel-shift
+// chains of 8 (one SHF per column) merged with byte permutes.
+template <int OFF, int N>
+__device__ __forceinline__ uint32_t pack_nonneg(const uint32_t (&v)[N]) {
+  uint32_t c[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int i = 7; i >= 0; --i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c[j] = __funnelshift_l(v[OFF + 8 * j + i], c[j], 1);
+  const uint32_t lo = __byte_perm(c[0], c[1], 0x0040);
+  const uint32_t hi = __byte_perm(c[2], c[3], 0x0040);
+  return ~__byte_perm(lo, hi, 0x5410);
 }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
   asm volatile(
@@ -421,11 +499,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
   } else if (warp == MMA_WARP) {
-    // ============ single-thread MMA issue (accumulators pre-loaded with bias) ============
-    if (lane == 0) {
+    // ============ MMA issue (accumulators pre-loaded with bias) ============
+    // The whole warp walks the schedule (all values warp-uniform); one
+    // elected lane issues (umma9_i8 / umma1_i8 / umma_commit_elect).
+    {
       const uint32_t sbo = 128;
       const uint32_t a_lbo = uint32_t(p.Q) * 16;
       const uint32_t b_lbo = uint32_t(p.n_tile) * 16;
+      const uint64_t pp = uint64_t(p.P);                        // one strip row, in 16-B units
+      const uint64_t bs = uint64_t(p.n_tile) * 2;               // one tap slab of B, in 16-B units
+      const uint64_t a_desc0 = umma_desc(smem_u32(a_base), a_lbo, sbo);
+      const uint64_t b_desc0 = umma_desc(smem_u32(b_base), b_lbo, sbo);
       int s = 0, ph = 0, it = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         const int ab = it & 1;
@@ -435,25 +519,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         for (int k = 0; k < p.kc; ++k) {
           mbar_wait(smem_u32(&full[s]), ph);
           tc_fence_after();
-          const uint32_t a_s = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
-          const uint32_t b_s = smem_u32(b_base + size_t(s) * p.b_stage_bytes);
+          // descriptors advance by address >> 4 (no carry out of the 14-bit field: smem < 256 KB)
+          const uint64_t a_s = a_desc0 + uint64_t((size_t(s) * p.a_stage_bytes) >> 4);
+          const uint64_t b_s = b_desc0 + uint64_t((size_t(s) * p.b_stage_bytes) >> 4);
           for (int b = 0; b < p.MB; ++b) {
-            const int q0 = block_q0(p, b);
-#pragma unroll
-            for (int tap = 0; tap < TAPS; ++tap) {
-              const int off = TAPS == 9 ? (tap / 3 - 1) * p.P + (tap % 3 - 1) : 0;
-              const uint64_t ad = umma_desc(a_s + uint32_t(q0 + off) * 16, a_lbo, sbo);
-              const uint64_t bd = umma_desc(b_s + uint32_t(tap * p.n_tile * 32), b_lbo, sbo);
-              umma_i8_acc(d0 + uint32_t(b * p.n_tile), ad, bd, p.idesc);
-            }
+            const uint64_t ad = a_s + uint64_t(block_q0(p, b));
+            if (TAPS == 9)
+              umma9_i8(d0 + uint32_t(b * p.n_tile), ad, b_s, pp, bs, p.idesc);
+            else
+              umma1_i8(d0 + uint32_t(b * p.n_tile), ad, b_s, p.idesc);
           }
-          umma_commit(smem_u32(&empty[s]));
+          umma_commit_elect(smem_u32(&empty[s]));
           if (++s == S) {
             s = 0;
             ph ^= 1;
           }
         }
-        umma_commit(smem_u32(&acc_full[ab]));
+        umma_commit_elect(smem_u32(&acc_full[ab]));
       }
     }
     __syncwarp();
@@ -545,17 +627,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           const int64_t opix = (int64_t(tl.nb) * p.ho + oy) * p.wo + ox;
           uint32_t w8[8];
 #pragma unroll
-          for (int rr = 0; rr < 8; ++rr) {
-            w8[rr] = 0u;
-            if (rr < rn.y) {
+          for (int rr = 0; rr < 8; ++rr) w8[rr] = 0u;
+          const uint32_t col0 = lane_base + uint32_t(ab * ACC_COLS + b * p.n_tile + rn.x * 32);
+          if (p.acc == nullptr) {
+            // two groups per TMEM load, one SHF per column to pack the signs
+#pragma unroll
+            for (int rr = 0; rr < 8; rr += 2) {
+              if (rr < rn.y) {
+                if (rr + 1 < rn.y) {
+                  uint32_t v[64];
+                  tmem_ld64(col0 + uint32_t(rr * 32), v);
+                  w8[rr] = pack_nonneg<0>(v);
+                  w8[rr + 1] = pack_nonneg<32>(v);
+                } else {
+                  uint32_t v[32];
+                  tmem_ld32(col0 + uint32_t(rr * 32), v);
+                  w8[rr] = pack_nonneg<0>(v);
+                }
+              }
+            }
+          } else {
+            // trace mode: also recover the reference accumulators
+#pragma unroll 1
+            for (int rr = 0; rr < rn.y; ++rr) {
               uint32_t v[32];
               const int gg = rn.x + rr;
-              tmem_ld32(lane_base + uint32_t(ab * ACC_COLS + b * p.n_tile + gg * 32), v);
-              uint32_t sgn = 0;
-#pragma unroll
-              for (int i = 0; i < 32; ++i) sgn |= (v[i] >> 31) << i;
-              w8[rr] = ~sgn;  // bit = D' >= 0
-              if (p.acc && valid) {
+              tmem_ld32(col0 + uint32_t(rr * 32), v);
+              w8[rr] = pack_nonneg<0>(v);
+              if (valid) {
                 const int oc = rn.z + 32 * rr;
                 const int jc = jt + 32 * gg;
                 int32_t *dst = p.acc + opix * p.c_out + oc;
