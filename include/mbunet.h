@@ -63,8 +63,10 @@ int mbu_last_path(void);
 /* Process-wide switches for cross-checking fast paths against exact ones.
  * MBU_OPT_GENERIC_ENDPOINTS: 1 = run stem/head through the all-float64
  * generic kernels instead of the float32-with-exact-recheck stem and the
- * specialised head (results must be identical). */
-enum { MBU_OPT_GENERIC_ENDPOINTS = 1 };
+ * specialised head (results must be identical).
+ * MBU_OPT_STEM_FFMA: 1 = run the stem through the float32 CUDA-core kernel
+ * instead of the tensor-core (bf16-split) kernel; both recheck in float64. */
+enum { MBU_OPT_GENERIC_ENDPOINTS = 1, MBU_OPT_STEM_FFMA = 2 };
 int mbu_set_option(int option, int value);
 
 /* ------------------------------------------------------------------ */

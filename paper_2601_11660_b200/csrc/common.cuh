@@ -22,6 +22,7 @@ int fail(int status, const std::string &msg);
 extern std::atomic<int64_t> g_launches;
 extern int g_last_path;
 extern int g_force_generic_fconv;  // mbu_set_option(MBU_OPT_GENERIC_ENDPOINTS)
+extern int g_force_stem_ffma;      // mbu_set_option(MBU_OPT_STEM_FFMA)
 
 inline int check_launch(const char *what) {
   cudaError_t e = cudaGetLastError();
@@ -108,6 +109,8 @@ struct mbu_fconv {
   int stem_fast = 0;          // float32 + exact-recheck stem kernel usable
   void *d_stem = nullptr;     // unused (kept for ABI of the struct)
   void *h_stem = nullptr;     // StemConsts host copy, passed as a kernel parameter
+  int stem_tc = 0;            // tensor-core stem usable (stem_tc.cu)
+  void *h_stem_tc = nullptr;  // StemTc: device B operand + margins
   int head_tab = 0;           // byte-table head usable (contiguous input lanes from 0)
   double *d_head_tab = nullptr;  // [c_out][ceil(c_in/8)][256] signed partial sums
 };
@@ -134,4 +137,9 @@ int launch_head_fast(const mbu_fconv *fc, const ActView &xb, int n, int h, int w
                      uint8_t *mask, cudaStream_t st);
 int head_prepare(mbu_fconv *fc, const double *w, const int32_t *lanes);
 void stem_free(mbu_fconv *fc);
+int stem_tc_prepare(mbu_fconv *fc, const double *w, const double *bias, const double *bn, double eps);
+void stem_tc_free(mbu_fconv *fc);
+bool stem_tc_usable(const mbu_fconv *fc, const double *x, int w);
+int launch_stem_tc(const mbu_fconv *fc, const double *x, int n, int h, int w, uint64_t *bits,
+                   int out_stride, int out_offset, cudaStream_t st);
 }  // namespace mbu

@@ -191,6 +191,8 @@ void stem_free(mbu_fconv *fc) {
 
 int launch_stem_fast(const mbu_fconv *fc, const double *x, int n, int h, int w, uint64_t *bits,
                      int out_stride, int out_offset, cudaStream_t st) {
+  if (!g_force_stem_ffma && stem_tc_usable(fc, x, w))
+    return launch_stem_tc(fc, x, n, h, w, bits, out_stride, out_offset, st);
   dim3 grid((w + STEM_TX - 1) / STEM_TX, (h + STEM_TY - 1) / STEM_TY, n);
   const int groups = ((fc->c_out + 127) / 128) * 4;
   const StemConsts &k = *static_cast<const StemConsts *>(fc->h_stem);

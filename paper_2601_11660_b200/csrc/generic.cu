@@ -26,6 +26,7 @@ static thread_local std::string t_last_error;
 std::atomic<int64_t> g_launches{0};
 int g_last_path = 0;
 int g_force_generic_fconv = 0;
+int g_force_stem_ffma = 0;
 
 void set_error(const std::string &msg) { t_last_error = msg; }
 int fail(int status, const std::string &msg) {
@@ -375,6 +376,10 @@ int mbu_set_option(int option, int value) {
     g_force_generic_fconv = value != 0;
     return MBU_OK;
   }
+  if (option == MBU_OPT_STEM_FFMA) {
+    g_force_stem_ffma = value != 0;
+    return MBU_OK;
+  }
   return fail(MBU_ERR_ENGINE, "unknown option " + std::to_string(option));
 }
 
@@ -537,6 +542,7 @@ int mbu_fconv_create(mbu_fconv **out, int device, int kh, int kw, int stride, in
   }
   if (st == MBU_OK && in_lanes) st = upload(&fc->d_lanes, in_lanes, size_t(c_in), "upload lanes");
   if (st == MBU_OK) st = stem_prepare(fc, weights, bias, bn, eps);
+  if (st == MBU_OK && fc->stem_fast) st = stem_tc_prepare(fc, weights, bias, bn, eps);
   if (st == MBU_OK && in_lanes) st = head_prepare(fc, weights, in_lanes);
   if (st != MBU_OK) {
     mbu_fconv_destroy(fc);
@@ -553,6 +559,7 @@ int mbu_fconv_destroy(mbu_fconv *fc) {
   cudaFree(fc->d_bn);
   cudaFree(fc->d_lanes);
   stem_free(fc);
+  stem_tc_free(fc);
   cudaFree(fc->d_head_tab);
   delete fc;
   return MBU_OK;

@@ -154,14 +154,31 @@ def test_bit_gemm_vs_numpy(cuda, rng):
     assert np.array_equal(mb.bit_gemm(a, pos, neg, 256), dense_a @ (pb - nb).T)
 
 
-def test_stem_fast_path_equals_float64_path(cuda):
-    """The float32 stem with exact float64 re-check must reproduce the
-    all-float64 kernel bit for bit, including pixels planted exactly on the
-    batchnorm decision boundary (which force the re-check)."""
-    import ctypes
-
+def _stem_bits(fc, x, cuda, mode):
+    """Run a stem FloatConvHandle in one of its three execution modes:
+    "tc" (tcgen05 bf16-split + float64 recheck), "ffma" (float32 CUDA cores +
+    float64 recheck) or "generic" (all float64)."""
     import torch
 
+    n, h, w, _ = x.shape
+    generic, ffma = {"tc": (0, 0), "ffma": (0, 1), "generic": (1, 0)}[mode]
+    _lib.call("mbu_set_option", 1, generic)
+    _lib.call("mbu_set_option", 2, ffma)
+    try:
+        out = torch.zeros((n, h, w, 2), dtype=torch.int64, device=cuda)
+        fc.run(n, h, w, x_f64=torch.from_numpy(x).to(cuda), bits=out)
+        torch.cuda.synchronize()
+    finally:
+        _lib.call("mbu_set_option", 1, 0)
+        _lib.call("mbu_set_option", 2, 0)
+    return out.cpu().numpy()
+
+
+def test_stem_fast_path_equals_float64_path(cuda):
+    """The tensor-core and float32 stems (both with exact float64 re-check)
+    must reproduce the all-float64 kernel bit for bit, including pixels
+    planted exactly on the batchnorm decision boundary (which force the
+    re-check), a non-finite input and a constant (gamma = 0) channel."""
     from paper_2601_11660_b200.ops import FloatConvHandle
 
     rng = np.random.default_rng(5)
@@ -179,17 +196,38 @@ def test_stem_fast_path_equals_float64_path(cuda):
     mean = acc[0, 17, 9, :] + be * sigma / np.where(g == 0, 1.0, g)  # boundary on a pixel
     spec = mb.ConvSpec(3, 3, 1, 1, 3, 64)
     fc = FloatConvHandle(w, b, spec, bn=(g, be, mean, v, eps))
-    xd = torch.from_numpy(x).to(cuda)
-    outs = []
-    for generic in (0, 1):
-        _lib.call("mbu_set_option", 1, generic)
-        out = torch.zeros((2, 40, 136, 2), dtype=torch.int64, device=cuda)
-        fc.run(2, 40, 136, x_f64=xd, bits=out)
-        torch.cuda.synchronize()
-        outs.append(out.cpu().numpy())
-    _lib.call("mbu_set_option", 1, 0)
-    assert np.array_equal(outs[0], outs[1])
+    outs = [_stem_bits(fc, x, cuda, m) for m in ("tc", "ffma", "generic")]
+    assert np.array_equal(outs[0], outs[2])
+    assert np.array_equal(outs[1], outs[2])
     ref = dense.ref_bn_sign(dense.ref_float_conv(x, w, b, 1, 1), g, be, mean, v, eps)
     got = mb.unpack_tensor(mb.BitTensor(2, 40, 136, 64, outs[0].view(np.uint64)))
     diff = got != ref
     assert diff.sum() <= 64, diff.sum()  # only planted exact-boundary pixels may round differently
+
+
+@pytest.mark.parametrize("shape", [(1, 37, 258), (2, 64, 128), (1, 5, 6)])
+def test_stem_tc_exact_ties(cuda, shape):
+    """Dyadic inputs and weights make the stem accumulator exact, and the
+    batchnorm means are set to accumulator values that occur, so a large
+    share of decisions lands exactly on (or one rounding away from) the
+    boundary: every one of them must be re-decided in float64 and agree with
+    the all-float64 kernel. Odd tile remainders (H % 4, W % 128) included."""
+    from paper_2601_11660_b200.ops import FloatConvHandle
+
+    rng = np.random.default_rng(77)
+    x = rng.integers(0, 8, size=shape + (3,)) / 8.0
+    w = rng.integers(-2, 3, size=(64, 3, 3, 3)) / 4.0
+    b = rng.integers(-4, 5, size=64) / 16.0
+    g = np.where(rng.random(64) < 0.5, 1.0, -1.0)
+    be = np.zeros(64)
+    v = np.ones(64)
+    acc = dense.ref_float_conv(x, w, b, 1, 1).reshape(-1, 64)
+    mean = acc[rng.integers(0, acc.shape[0], 64), np.arange(64)]
+    mean[::7] += 2.0 ** -40  # one rounding away from a reachable value
+    fc = FloatConvHandle(w, b, mb.ConvSpec(3, 3, 1, 1, 3, 64), bn=(g, be, mean, v, 0.0))
+    tc = _stem_bits(fc, x, cuda, "tc")
+    gen = _stem_bits(fc, x, cuda, "generic")
+    assert np.array_equal(tc, gen)
+    ref = dense.ref_bn_sign(dense.ref_float_conv(x, w, b, 1, 1), g, be, mean, v, 0.0)
+    got = mb.unpack_tensor(mb.BitTensor(*shape, 64, tc.view(np.uint64)))
+    assert np.array_equal(got, ref)
