@@ -69,7 +69,7 @@ def load(path: str | os.PathLike | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("MBU_LIB", LIB_PATH))
     if not p.exists():
         raise EngineError(
             f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"

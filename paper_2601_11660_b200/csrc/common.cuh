@@ -90,8 +90,7 @@ struct mbu_conv {
   int n_tile = 0;                // N per CTA tile
   int n_tiles = 0;
   int kc = 0;                    // active 32-lane chunks per pixel
-  int chunks_per_stage = 0;      // 32-lane chunks per pipeline stage
-  int n_stages_k = 0;            // K stages per tile (= ceil(kc / chunks_per_stage))
+  int chunk_consec = 0;          // bit i: chunk groups of 2^i are consecutive aligned words
   int32_t *d_chunk_word = nullptr;  // [kc] u32 index inside a pixel for each chunk
   int8_t *d_b = nullptr;         // repacked s8 weights, UMMA K-major core-matrix order
   void *d_thr2 = nullptr;        // int2 per GEMM column: bit = (m * acc >= t)

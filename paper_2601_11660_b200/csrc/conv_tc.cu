@@ -72,8 +72,9 @@ constexpr int MAX_CHUNKS = 64;  // 32-lane chunks per pixel (2048 lanes)
 constexpr int SMEM_HEADER = 1024;
 constexpr int MIN_SMEM = 120 * 1024;  // > half an SM: exactly one CTA (and TMEM owner) per SM
 constexpr int PROD_ITEMS = 6;         // strip rows per producer thread per stage (Q <= 6*256)
-constexpr int LOOKAHEAD = 4;          // raw-bit stages in flight per producer thread
-constexpr int RAW_STAGES = LOOKAHEAD + 1;
+// raw-bit stages in flight per producer thread (template LA): 4 for the 3x3
+// conv (each stage feeds nine taps), 8 for 1x1 / tconv (one tap per stage)
+constexpr int LA_CONV3 = 4, LA_TAP1 = 8;
 
 struct Params {
   const uint32_t *x32;
@@ -83,7 +84,10 @@ struct Params {
   uint32_t p_magic;         // ceil(2^32 / P): q / P == umulhi(q, p_magic) for q < 2^16
   int col_tiles, row_tiles, n_tiles, num_tiles;
   int u8_act;               // 1: A = bits as u8 {0,1} (neg_one); 0: s8 {-1,0,+1} (zero pad)
-  int kc;
+  int kc;                   // active 32-lane chunks per pixel
+  int ks;                   // K stages per tile = kc / cps
+  int vec;                  // raw chunks of a stage are consecutive, aligned words
+  uint32_t a_chunk_bytes;   // A bytes of one chunk inside a stage (Q * 32)
   const int32_t *chunk_word;
   const int8_t *b;
   int n_tile;
@@ -328,8 +332,9 @@ __device__ __forceinline__ Run run_at(const Params &p, int jt, int g, int groups
 }
 
 // ------------------------------------------------------------------ kernel
-template <int TAPS, bool TCONV>
+template <int TAPS, bool TCONV, int LA, int CPS>
 __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_constant__ Params p) {
+  constexpr int RAW_STAGES = LA + 1;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
   uint64_t *empty = full + MAX_STAGES;
@@ -358,7 +363,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
   for (int i = threadIdx.x; i < p.kc; i += blockDim.x) chunk_s[i] = p.chunk_word[i];
   // per-N-tile epilogue runs and per-column TMEM biases, staged once per CTA
   int4 *runs_s = reinterpret_cast<int4 *>(b_base + size_t(p.stages) * p.b_stage_bytes +
-                                          size_t(RAW_STAGES) * p.Q * 4);
+                                          size_t(RAW_STAGES) * p.Q * CPS * 4);
   int32_t *bias_s = reinterpret_cast<int32_t *>(runs_s + p.n_tiles * 8);
   for (int i = threadIdx.x; i < p.n_tiles * p.n_tile; i += blockDim.x) bias_s[i] = p.col_bias[i];
   if (threadIdx.x < p.n_tiles) {
@@ -419,75 +424,134 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       }
       c.t = t;
     };
-    // stage g <-> (tile blockIdx.x + (g / kc) * gridDim.x, chunk g % kc)
+    // stage g <-> (tile blockIdx.x + (g / ks) * gridDim.x, chunks [cps*(g % ks), +cps))
     const int tiles_here = p.num_tiles > int(blockIdx.x)
                                ? (p.num_tiles - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x)
                                : 0;
-    const int n_stages_total = tiles_here * p.kc;
+    const int n_stages_total = tiles_here * p.ks;
+    constexpr int cps = CPS;
+    const int slot_words = p.Q * cps;
     // incremental cursors (no integer division in the per-stage loop)
     int i_t = blockIdx.x, i_k = 0, i_slot = 0, i_g = 0;        // issue side
     int e_t = blockIdx.x, e_k = 0, e_slot = 0, s = 0, ph = 0;  // expand side
     auto issue = [&]() {
       if (i_g < n_stages_total) {
         if (i_t != ic.t) tile_offsets(ic, i_t);
-        const int cw = chunk_s[i_k];
-        uint32_t *dst = raw + i_slot * p.Q;
+        const int k0 = i_k * cps;
+        const int cw = chunk_s[k0];  // (read once: the cp.async asm clobbers memory)
+        uint32_t *dst = raw + i_slot * slot_words;
 #pragma unroll
         for (int j = 0; j < PROD_ITEMS; ++j) {
           const int q = pt + j * PROD_THREADS;
           if (q < p.Q) {
             const bool in = (ic.inb >> j) & 1;
-            const uint32_t *src = p.x32 + (in ? ic.off[j] + cw : 0);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst + q)),
-                         "l"(src), "r"(in ? 4 : 0)
-                         : "memory");
+            const uint32_t d = smem_u32(dst + q * cps);
+            if constexpr (cps == 1) {
+              const uint32_t *src = p.x32 + (in ? ic.off[j] + cw : 0);
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src),
+                           "r"(in ? 4 : 0)
+                           : "memory");
+            } else if (p.vec) {  // cps consecutive words, one copy (zero-filled out of bounds)
+              const uint32_t *src = p.x32 + (in ? ic.off[j] + cw : 0);
+              if constexpr (cps == 4)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src),
+                             "r"(in ? 16 : 0)
+                             : "memory");
+              else if constexpr (cps == 2)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src),
+                             "r"(in ? 8 : 0)
+                             : "memory");
+              else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src),
+                             "r"(in ? 4 : 0)
+                             : "memory");
+            } else {
+#pragma unroll
+              for (int c = 0; c < cps; ++c) {
+                const uint32_t *src = p.x32 + (in ? ic.off[j] + chunk_s[k0 + c] : 0);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d + 4 * c), "l"(src),
+                             "r"(in ? 4 : 0)
+                             : "memory");
+              }
+            }
           }
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group
       ++i_g;
-      if (++i_k == p.kc) {
+      if (++i_k == p.ks) {
         i_k = 0;
         i_t += gridDim.x;
       }
       if (++i_slot == RAW_STAGES) i_slot = 0;
     };
 #pragma unroll 1
-    for (int g = 0; g < LOOKAHEAD; ++g) issue();
+    for (int g = 0; g < LA; ++g) issue();
     for (int g = 0; g < n_stages_total; ++g) {
       issue();
-      asm volatile("cp.async.wait_group %0;" ::"n"(LOOKAHEAD) : "memory");  // group g landed
+      asm volatile("cp.async.wait_group %0;" ::"n"(LA) : "memory");  // group g landed
       if (e_t != ec.t) tile_offsets(ec, e_t);
-      const uint32_t *rw = raw + e_slot * p.Q;
+      const uint32_t *rw = raw + e_slot * slot_words;
       if (g >= S) mbar_wait(smem_u32(&empty[s]), ph ^ 1);
-      const uint32_t a0 = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
-      const uint32_t a1 = a0 + p.Q * 16;
+      const uint32_t a_st = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
+      if constexpr (cps == 1) {
+        const uint32_t a0 = a_st;
+        const uint32_t a1 = a0 + p.Q * 16;
 #pragma unroll
-      for (int j = 0; j < PROD_ITEMS; ++j) {
-        const int q = pt + j * PROD_THREADS;
-        if (q < p.Q) {
-          const uint32_t b = rw[q];
-          if ((ec.inb >> j) & 1) {
-            if (p.u8_act) {
-              sts128(a0 + q * 16, spread4(b & 0xF), spread4((b >> 4) & 0xF),
-                     spread4((b >> 8) & 0xF), spread4((b >> 12) & 0xF));
-              sts128(a1 + q * 16, spread4((b >> 16) & 0xF), spread4((b >> 20) & 0xF),
-                     spread4((b >> 24) & 0xF), spread4(b >> 28));
-            } else {
-              sts128(a0 + q * 16, pm4(b & 0xF), pm4((b >> 4) & 0xF), pm4((b >> 8) & 0xF),
-                     pm4((b >> 12) & 0xF));
-              sts128(a1 + q * 16, pm4((b >> 16) & 0xF), pm4((b >> 20) & 0xF),
-                     pm4((b >> 24) & 0xF), pm4(b >> 28));
+        for (int j = 0; j < PROD_ITEMS; ++j) {
+          const int q = pt + j * PROD_THREADS;
+          if (q < p.Q) {
+            const uint32_t b = rw[q];
+            if ((ec.inb >> j) & 1) {
+              if (p.u8_act) {
+                sts128(a0 + q * 16, spread4(b & 0xF), spread4((b >> 4) & 0xF),
+                       spread4((b >> 8) & 0xF), spread4((b >> 12) & 0xF));
+                sts128(a1 + q * 16, spread4((b >> 16) & 0xF), spread4((b >> 20) & 0xF),
+                       spread4((b >> 24) & 0xF), spread4(b >> 28));
+              } else {
+                sts128(a0 + q * 16, pm4(b & 0xF), pm4((b >> 4) & 0xF), pm4((b >> 8) & 0xF),
+                       pm4((b >> 12) & 0xF));
+                sts128(a1 + q * 16, pm4((b >> 16) & 0xF), pm4((b >> 20) & 0xF),
+                       pm4((b >> 24) & 0xF), pm4(b >> 28));
+              }
+            } else {  // out of bounds: a' = 0, i.e. -1 (u8, neg_one) / a = 0 (s8, zero pad)
+              sts128(a0 + q * 16, 0u, 0u, 0u, 0u);
+              sts128(a1 + q * 16, 0u, 0u, 0u, 0u);
             }
-          } else {  // out of bounds: a' = 0, i.e. -1 (u8, neg_one) / a = 0 (s8, zero pad)
-            sts128(a0 + q * 16, 0u, 0u, 0u, 0u);
-            sts128(a1 + q * 16, 0u, 0u, 0u, 0u);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < PROD_ITEMS; ++j) {
+          const int q = pt + j * PROD_THREADS;
+          if (q < p.Q) {
+#pragma unroll
+            for (int c = 0; c < cps; ++c) {
+              const uint32_t a0 = a_st + c * p.a_chunk_bytes + q * 16;
+              const uint32_t a1 = a0 + p.Q * 16;
+              const uint32_t b = rw[q * cps + c];
+              if ((ec.inb >> j) & 1) {
+                if (p.u8_act) {
+                  sts128(a0, spread4(b & 0xF), spread4((b >> 4) & 0xF), spread4((b >> 8) & 0xF),
+                         spread4((b >> 12) & 0xF));
+                  sts128(a1, spread4((b >> 16) & 0xF), spread4((b >> 20) & 0xF),
+                         spread4((b >> 24) & 0xF), spread4(b >> 28));
+                } else {
+                  sts128(a0, pm4(b & 0xF), pm4((b >> 4) & 0xF), pm4((b >> 8) & 0xF), pm4((b >> 12) & 0xF));
+                  sts128(a1, pm4((b >> 16) & 0xF), pm4((b >> 20) & 0xF), pm4((b >> 24) & 0xF),
+                         pm4(b >> 28));
+                }
+              } else {
+                sts128(a0, 0u, 0u, 0u, 0u);
+                sts128(a1, 0u, 0u, 0u, 0u);
+              }
+            }
           }
         }
       }
       fence_proxy_async();
       mbar_arrive(smem_u32(&full[s]));
-      if (++e_k == p.kc) {
+      if (++e_k == p.ks) {
         e_k = 0;
         e_t += gridDim.x;
       }
@@ -516,18 +580,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         mbar_wait(smem_u32(&acc_empty[ab]), (it >> 1) & 1);
         tc_fence_after();
         const uint32_t d0 = tmem + uint32_t(ab * ACC_COLS);
-        for (int k = 0; k < p.kc; ++k) {
+        for (int k = 0; k < p.ks; ++k) {
           mbar_wait(smem_u32(&full[s]), ph);
           tc_fence_after();
           // descriptors advance by address >> 4 (no carry out of the 14-bit field: smem < 256 KB)
           const uint64_t a_s = a_desc0 + uint64_t((size_t(s) * p.a_stage_bytes) >> 4);
           const uint64_t b_s = b_desc0 + uint64_t((size_t(s) * p.b_stage_bytes) >> 4);
-          for (int b = 0; b < p.MB; ++b) {
-            const uint64_t ad = a_s + uint64_t(block_q0(p, b));
-            if (TAPS == 9)
-              umma9_i8(d0 + uint32_t(b * p.n_tile), ad, b_s, pp, bs, p.idesc);
-            else
-              umma1_i8(d0 + uint32_t(b * p.n_tile), ad, b_s, p.idesc);
+          if (TAPS == 9) {
+            for (int b = 0; b < p.MB; ++b)
+              umma9_i8(d0 + uint32_t(b * p.n_tile), a_s + uint64_t(block_q0(p, b)), b_s, pp, bs, p.idesc);
+          } else {
+#pragma unroll
+            for (int c = 0; c < CPS; ++c)  // chunk c: A region c, B slab c
+              for (int b = 0; b < p.MB; ++b)
+                umma1_i8(d0 + uint32_t(b * p.n_tile),
+                         a_s + uint64_t(c * (p.a_chunk_bytes >> 4)) + uint64_t(block_q0(p, b)),
+                         b_s + uint64_t(c) * bs, p.idesc);
           }
           umma_commit_elect(smem_u32(&empty[s]));
           if (++s == S) {
@@ -545,8 +613,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       int s = 0, ph = 0, g = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
         const int nt = t % p.n_tiles;
-        const int8_t *src = p.b + size_t(nt) * p.kc * p.b_stage_bytes;
-        for (int k = 0; k < p.kc; ++k, ++g) {
+        const int8_t *src = p.b + size_t(nt) * p.ks * p.b_stage_bytes;
+        for (int k = 0; k < p.ks; ++k, ++g) {
           if (g >= S) mbar_wait(smem_u32(&empty[s]), ph ^ 1);
           const uint32_t bar = smem_u32(&full[s]);
           mbar_arrive_expect_tx(bar, p.b_stage_bytes);
@@ -723,14 +791,30 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
   std::vector<uint8_t> real(lpp, 0);
   for (int i = 0; i < n_seg; ++i)
     for (int l = seg_off[i]; l < seg_off[i] + seg_cnt[i]; ++l) real[l] = 1;
+  // 3x3: every 32-lane chunk holding a real lane. One tap (1x1, tconv): every
+  // chunk of each 128-lane block holding a real lane, so four chunks (16 B of
+  // a pixel) form one pipeline stage; pad lanes carry zero weights.
+  const int gran = (conv3 ? 32 : 128);
   std::vector<int32_t> chunk_word;
-  for (int c = 0; c < n_chunks; ++c) {
+  for (int g0 = 0; g0 < lpp; g0 += gran) {
     bool any = false;
-    for (int l = 32 * c; l < 32 * c + 32; ++l) any |= real[l] != 0;
-    if (any) chunk_word.push_back(c);
+    for (int l = g0; l < g0 + gran; ++l) any |= real[l] != 0;
+    if (any)
+      for (int c = g0 / 32; c < (g0 + gran) / 32; ++c) chunk_word.push_back(c);
   }
   const int kc = int(chunk_word.size());
   if (kc == 0 || kc > tc::MAX_CHUNKS) return MBU_OK;
+  // bit i: groups of 2^i chunks are consecutive, 2^i-aligned words (one vector copy)
+  cv->chunk_consec = 0;
+  for (int i = 0; i < 3; ++i) {
+    const int g = 1 << i;
+    bool ok = kc % g == 0;
+    for (int k0 = 0; ok && k0 < kc; k0 += g) {
+      ok = chunk_word[k0] % g == 0;
+      for (int j = 1; ok && j < g; ++j) ok = chunk_word[k0 + j] == chunk_word[k0] + j;
+    }
+    if (ok) cv->chunk_consec |= 1 << i;
+  }
   const int taps = cv->transposed ? 1 : cv->kh * cv->kw;
   const int s2 = cv->transposed ? cv->stride * cv->stride : 1;
   const int c_out_pad = (cv->c_out + 31) / 32 * 32;
@@ -861,16 +945,16 @@ static int num_sms() {
   return sms;
 }
 
-template <int TAPS, bool TCONV>
+template <int TAPS, bool TCONV, int LA, int CPS>
 static int launch_tc_impl(const tc::Params &p, int grid, size_t smem, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    MBU_TRY(check_cuda(cudaFuncSetAttribute(tc::conv_tc_kernel<TAPS, TCONV>,
+    MBU_TRY(check_cuda(cudaFuncSetAttribute(tc::conv_tc_kernel<TAPS, TCONV, LA, CPS>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
                        "cudaFuncSetAttribute"));
     configured = true;
   }
-  tc::conv_tc_kernel<TAPS, TCONV><<<grid, tc::NUM_THREADS, smem, st>>>(p);
+  tc::conv_tc_kernel<TAPS, TCONV, LA, CPS><<<grid, tc::NUM_THREADS, smem, st>>>(p);
   return check_launch("conv_tc_kernel");
 }
 
@@ -914,11 +998,18 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   if (Q > tc::PROD_ITEMS * tc::PROD_THREADS)
     return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv strip taller than the producer tiling");
   p.Q = Q;
-  p.a_stage_bytes = uint32_t((size_t(Q) * 32 + 1023) / 1024 * 1024);
-  p.b_stage_bytes = uint32_t(cv->b_stage_bytes);
+  // one-tap convs pack four 32-lane chunks (a 128-lane block) into a stage
+  const int cps = cv->taps == 1 ? 4 : 1;
+  if (cv->kc % cps) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 one-tap conv needs whole 128-lane blocks");
+  p.ks = cv->kc / cps;
+  p.vec = ((cv->chunk_consec >> (cps >> 1)) & 1) && p.x_stride32 % cps == 0 && p.x_off32 % cps == 0;
+  p.a_chunk_bytes = uint32_t(Q) * 32;
+  p.a_stage_bytes = uint32_t((size_t(Q) * 32 * cps + 1023) / 1024 * 1024);
+  p.b_stage_bytes = uint32_t(cv->b_stage_bytes * cps);
   const size_t stage = size_t(p.a_stage_bytes) + p.b_stage_bytes;
+  const int raw_stages = (cv->taps == 9 ? tc::LA_CONV3 : tc::LA_TAP1) + 1;
   // raw-bit ring + per-N-tile run table + per-column biases
-  const size_t raw_bytes = size_t(tc::RAW_STAGES) * Q * 4 + size_t(cv->n_tiles) * 8 * 16 +
+  const size_t raw_bytes = size_t(raw_stages) * Q * cps * 4 + size_t(cv->n_tiles) * 8 * 16 +
                            size_t(cv->n_tiles) * cv->n_tile * 4;
   int stages = int((227 * 1024 - tc::SMEM_HEADER - raw_bytes) / stage);
   if (stages < 2) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv stage does not fit in shared memory");
@@ -952,9 +1043,9 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   const int grid = int(std::min<int64_t>(tiles, num_sms()));
   size_t smem = tc::SMEM_HEADER + size_t(p.stages) * stage + raw_bytes;
   smem = std::max<size_t>(smem, tc::MIN_SMEM);
-  if (cv->transposed) return launch_tc_impl<1, true>(p, grid, smem, st);
-  if (cv->taps == 9) return launch_tc_impl<9, false>(p, grid, smem, st);
-  return launch_tc_impl<1, false>(p, grid, smem, st);
+  if (cv->transposed) return launch_tc_impl<1, true, tc::LA_TAP1, 4>(p, grid, smem, st);
+  if (cv->taps == 9) return launch_tc_impl<9, false, tc::LA_CONV3, 1>(p, grid, smem, st);
+  return launch_tc_impl<1, false, tc::LA_TAP1, 4>(p, grid, smem, st);
 }
 
 }  // namespace mbu
