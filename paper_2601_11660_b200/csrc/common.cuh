@@ -94,7 +94,10 @@ struct mbu_conv {
   int32_t *d_chunk_word = nullptr;  // [kc] u32 index inside a pixel for each chunk
   int8_t *d_b = nullptr;         // repacked s8 weights, UMMA K-major core-matrix order
   void *d_thr2 = nullptr;        // int2 per GEMM column: bit = (m * acc >= t)
-  size_t b_stage_bytes = 0;      // bytes of B per (n tile, K stage)
+  size_t b_stage_bytes = 0;      // bytes of B per (n tile, 32-lane chunk)
+  int n_slabs = 0;               // one-tap layers: distinct MMA bias slabs (0 = TMEM init)
+  int8_t *d_bias_slab = nullptr;
+  int32_t *d_slab_of_nt = nullptr;
 };
 
 struct mbu_fconv {

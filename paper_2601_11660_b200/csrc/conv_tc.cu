@@ -71,7 +71,9 @@ constexpr int MAX_STAGES = 8;
 constexpr int MAX_CHUNKS = 64;  // 32-lane chunks per pixel (2048 lanes)
 constexpr int SMEM_HEADER = 1024;
 constexpr int MIN_SMEM = 120 * 1024;  // > half an SM: exactly one CTA (and TMEM owner) per SM
-constexpr int PROD_ITEMS = 6;         // strip rows per producer thread per stage (Q <= 6*256)
+// strip rows per producer thread per stage: Q <= 6*256 for the 3x3 conv, <= 2*256 for one tap
+constexpr int PROD_ITEMS = 6;
+constexpr int prod_items(int taps) { return taps == 9 ? 6 : 2; }
 // raw-bit stages in flight per producer thread (template LA): 4 for the 3x3
 // conv (each stage feeds nine taps), 8 for 1x1 / tconv (one tap per stage)
 constexpr int LA_CONV3 = 4, LA_TAP1 = 8;
@@ -100,6 +102,13 @@ struct Params {
   int32_t *acc;
   uint32_t *bits;
   int out_stride32, out_off32, out_groups;
+  // shared-memory layout (byte offsets, computed on the host)
+  uint32_t off_b, off_raw, off_runs, off_ones, off_slab, off_slabmap;
+  int b_resident;           // all weights resident in smem (loaded once), no B stream
+  int mma_bias;             // bias enters the accumulator by an MMA (ones x bias slab)
+  int n_slabs;
+  const int8_t *bias_slab;  // [n_slabs][khalf][n_tile][16]: s8, sum(lo) + 127*sum(hi) = bias
+  const int32_t *slab_of_nt;
   const int32_t *col_bias;  // per GEMM column: TMEM init value
   const int32_t *col_sgn;   // per GEMM column: +-1
   const int32_t *col_w;     // per GEMM column: W (u8 mode) or 0
@@ -212,6 +221,16 @@ __device__ __forceinline__ void umma1_i8(uint32_t tmem_d, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc)
       : "memory");
 }
+// overwrite form (accumulate = 0): the bias MMA that opens a tile
+__device__ __forceinline__ void umma1_i8_first(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, 0, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc)
+      : "memory");
+}
 __device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -285,7 +304,10 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
 // 4 activation bits -> 4 bytes. u8 mode: bit -> 0x00/0x01. s8 mode: bit 1 ->
 // 0x01 (+1), bit 0 -> 0xFF (-1).
 __device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
-__device__ __forceinline__ uint32_t pm4(uint32_t nib) { return ~(spread4(nib) * 0xFEu); }
+// u8 mode (mul 1, xr 0): 0x00 / 0x01; s8 mode (mul 0xFE, xr ~0): 0xFF / 0x01
+__device__ __forceinline__ uint32_t exp4(uint32_t nib, uint32_t mul, uint32_t xr) {
+  return (spread4(nib) * mul) ^ xr;
+}
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
                                        uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
@@ -335,15 +357,17 @@ __device__ __forceinline__ Run run_at(const Params &p, int jt, int g, int groups
 template <int TAPS, bool TCONV, int LA, int CPS>
 __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_constant__ Params p) {
   constexpr int RAW_STAGES = LA + 1;
+  constexpr int PI = prod_items(TAPS);
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
   uint64_t *empty = full + MAX_STAGES;
   uint64_t *acc_full = empty + MAX_STAGES;
   uint64_t *acc_empty = acc_full + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
+  uint64_t *bres = acc_empty + 2;  // resident weights landed
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bres + 1);
   int32_t *chunk_s = reinterpret_cast<int32_t *>(smem + 512);  // MAX_CHUNKS words
   uint8_t *a_base = smem + SMEM_HEADER;
-  uint8_t *b_base = a_base + size_t(p.stages) * p.a_stage_bytes;
+  uint8_t *b_base = smem + p.off_b;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -351,9 +375,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(smem_u32(&full[s]), PROD_THREADS + 1);
+      mbar_init(smem_u32(&full[s]), PROD_THREADS + (p.b_resident ? 0 : 1));
       mbar_init(smem_u32(&empty[s]), 1);
     }
+    mbar_init(smem_u32(bres), 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
       mbar_init(smem_u32(&acc_empty[i]), EPI_THREADS);
@@ -362,8 +387,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
   }
   for (int i = threadIdx.x; i < p.kc; i += blockDim.x) chunk_s[i] = p.chunk_word[i];
   // per-N-tile epilogue runs and per-column TMEM biases, staged once per CTA
-  int4 *runs_s = reinterpret_cast<int4 *>(b_base + size_t(p.stages) * p.b_stage_bytes +
-                                          size_t(RAW_STAGES) * p.Q * CPS * 4);
+  int4 *runs_s = reinterpret_cast<int4 *>(smem + p.off_runs);
   int32_t *bias_s = reinterpret_cast<int32_t *>(runs_s + p.n_tiles * 8);
   for (int i = threadIdx.x; i < p.n_tiles * p.n_tile; i += blockDim.x) bias_s[i] = p.col_bias[i];
   if (threadIdx.x < p.n_tiles) {
@@ -377,6 +401,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       g += rn.len;
     }
     for (; r < 8; ++r) runs_s[nt * 8 + r] = make_int4(0, 0, 0, 0);
+  }
+  if (p.mma_bias) {  // ones slab (16 x 1, 16 x 127 per row) + bias slabs, read by the tensor core
+    uint4 *ones = reinterpret_cast<uint4 *>(smem + p.off_ones);
+    for (int i = threadIdx.x; i < 256; i += blockDim.x)
+      ones[i] = i < 128 ? make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u)
+                        : make_uint4(0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu);
+    uint4 *slab = reinterpret_cast<uint4 *>(smem + p.off_slab);
+    const uint4 *src = reinterpret_cast<const uint4 *>(p.bias_slab);
+    for (int i = threadIdx.x; i < p.n_slabs * p.n_tile * 2; i += blockDim.x) slab[i] = src[i];
+    int32_t *smap = reinterpret_cast<int32_t *>(smem + p.off_slabmap);
+    for (int i = threadIdx.x; i < p.n_tiles; i += blockDim.x) smap[i] = p.slab_of_nt[i];
+    fence_proxy_async();
   }
   if (warp == MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -403,10 +439,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     // offsets of its strip rows and an in-bounds mask.
     const int pt = threadIdx.x - PROD_WARP0 * 32;
     const int strip_rows = p.R + 2 * p.halo;
-    uint32_t *raw = reinterpret_cast<uint32_t *>(b_base + size_t(p.stages) * p.b_stage_bytes);
+    uint32_t *raw = reinterpret_cast<uint32_t *>(smem + p.off_raw);
     struct Cache {
       int t = -1;
-      int off[PROD_ITEMS];
+      int off[PI];
       uint32_t inb = 0;
     };
     Cache ic, ec;  // issue-side and expand-side tile caches
@@ -414,7 +450,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       const Tile tl = decode_tile(p, t);
       c.inb = 0;
 #pragma unroll
-      for (int j = 0; j < PROD_ITEMS; ++j) {
+      for (int j = 0; j < PI; ++j) {
         const int q = pt + j * PROD_THREADS;
         const int rr = int(__umulhi(uint32_t(q), p.p_magic));
         const int iy = tl.y0 - p.halo + rr;
@@ -431,6 +467,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     const int n_stages_total = tiles_here * p.ks;
     constexpr int cps = CPS;
     const int slot_words = p.Q * cps;
+    const uint32_t emul = p.u8_act ? 1u : 0xFEu, exr = p.u8_act ? 0u : 0xFFFFFFFFu;
     // incremental cursors (no integer division in the per-stage loop)
     int i_t = blockIdx.x, i_k = 0, i_slot = 0, i_g = 0;        // issue side
     int e_t = blockIdx.x, e_k = 0, e_slot = 0, s = 0, ph = 0;  // expand side
@@ -441,7 +478,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         const int cw = chunk_s[k0];  // (read once: the cp.async asm clobbers memory)
         uint32_t *dst = raw + i_slot * slot_words;
 #pragma unroll
-        for (int j = 0; j < PROD_ITEMS; ++j) {
+        for (int j = 0; j < PI; ++j) {
           const int q = pt + j * PROD_THREADS;
           if (q < p.Q) {
             const bool in = (ic.inb >> j) & 1;
@@ -498,7 +535,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         const uint32_t a0 = a_st;
         const uint32_t a1 = a0 + p.Q * 16;
 #pragma unroll
-        for (int j = 0; j < PROD_ITEMS; ++j) {
+        for (int j = 0; j < PI; ++j) {
           const int q = pt + j * PROD_THREADS;
           if (q < p.Q) {
             const uint32_t b = rw[q];
@@ -509,10 +546,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
                 sts128(a1 + q * 16, spread4((b >> 16) & 0xF), spread4((b >> 20) & 0xF),
                        spread4((b >> 24) & 0xF), spread4(b >> 28));
               } else {
-                sts128(a0 + q * 16, pm4(b & 0xF), pm4((b >> 4) & 0xF), pm4((b >> 8) & 0xF),
-                       pm4((b >> 12) & 0xF));
-                sts128(a1 + q * 16, pm4((b >> 16) & 0xF), pm4((b >> 20) & 0xF),
-                       pm4((b >> 24) & 0xF), pm4(b >> 28));
+                sts128(a0 + q * 16, exp4(b & 0xF, 0xFEu, ~0u), exp4((b >> 4) & 0xF, 0xFEu, ~0u),
+                       exp4((b >> 8) & 0xF, 0xFEu, ~0u), exp4((b >> 12) & 0xF, 0xFEu, ~0u));
+                sts128(a1 + q * 16, exp4((b >> 16) & 0xF, 0xFEu, ~0u), exp4((b >> 20) & 0xF, 0xFEu, ~0u),
+                       exp4((b >> 24) & 0xF, 0xFEu, ~0u), exp4(b >> 28, 0xFEu, ~0u));
               }
             } else {  // out of bounds: a' = 0, i.e. -1 (u8, neg_one) / a = 0 (s8, zero pad)
               sts128(a0 + q * 16, 0u, 0u, 0u, 0u);
@@ -522,7 +559,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < PROD_ITEMS; ++j) {
+        for (int j = 0; j < PI; ++j) {
           const int q = pt + j * PROD_THREADS;
           if (q < p.Q) {
 #pragma unroll
@@ -531,16 +568,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
               const uint32_t a1 = a0 + p.Q * 16;
               const uint32_t b = rw[q * cps + c];
               if ((ec.inb >> j) & 1) {
-                if (p.u8_act) {
-                  sts128(a0, spread4(b & 0xF), spread4((b >> 4) & 0xF), spread4((b >> 8) & 0xF),
-                         spread4((b >> 12) & 0xF));
-                  sts128(a1, spread4((b >> 16) & 0xF), spread4((b >> 20) & 0xF),
-                         spread4((b >> 24) & 0xF), spread4(b >> 28));
-                } else {
-                  sts128(a0, pm4(b & 0xF), pm4((b >> 4) & 0xF), pm4((b >> 8) & 0xF), pm4((b >> 12) & 0xF));
-                  sts128(a1, pm4((b >> 16) & 0xF), pm4((b >> 20) & 0xF), pm4((b >> 24) & 0xF),
-                         pm4(b >> 28));
-                }
+                sts128(a0, exp4(b & 0xF, emul, exr), exp4((b >> 4) & 0xF, emul, exr),
+                       exp4((b >> 8) & 0xF, emul, exr), exp4((b >> 12) & 0xF, emul, exr));
+                sts128(a1, exp4((b >> 16) & 0xF, emul, exr), exp4((b >> 20) & 0xF, emul, exr),
+                       exp4((b >> 24) & 0xF, emul, exr), exp4(b >> 28, emul, exr));
               } else {
                 sts128(a0, 0u, 0u, 0u, 0u);
                 sts128(a1, 0u, 0u, 0u, 0u);
@@ -574,18 +605,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       const uint64_t bs = uint64_t(p.n_tile) * 2;               // one tap slab of B, in 16-B units
       const uint64_t a_desc0 = umma_desc(smem_u32(a_base), a_lbo, sbo);
       const uint64_t b_desc0 = umma_desc(smem_u32(b_base), b_lbo, sbo);
+      const uint64_t ones_desc = umma_desc(smem_u32(smem + p.off_ones), 128 * 16, sbo);
+      const uint64_t slab_desc0 = umma_desc(smem_u32(smem + p.off_slab), b_lbo, sbo);
+      const int32_t *smap = reinterpret_cast<const int32_t *>(smem + p.off_slabmap);
+      if (p.b_resident) mbar_wait(smem_u32(bres), 0);
       int s = 0, ph = 0, it = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         const int ab = it & 1;
+        const int nt = t % p.n_tiles;
         mbar_wait(smem_u32(&acc_empty[ab]), (it >> 1) & 1);
         tc_fence_after();
         const uint32_t d0 = tmem + uint32_t(ab * ACC_COLS);
+        if (p.mma_bias) {
+          const uint64_t sd = slab_desc0 + uint64_t(smap[nt]) * uint64_t(p.n_tile * 2);
+          for (int b = 0; b < p.MB; ++b) umma1_i8_first(d0 + uint32_t(b * p.n_tile), ones_desc, sd, p.idesc);
+        }
         for (int k = 0; k < p.ks; ++k) {
           mbar_wait(smem_u32(&full[s]), ph);
           tc_fence_after();
           // descriptors advance by address >> 4 (no carry out of the 14-bit field: smem < 256 KB)
           const uint64_t a_s = a_desc0 + uint64_t((size_t(s) * p.a_stage_bytes) >> 4);
-          const uint64_t b_s = b_desc0 + uint64_t((size_t(s) * p.b_stage_bytes) >> 4);
+          const uint64_t b_s =
+              b_desc0 + uint64_t(((p.b_resident ? size_t(nt * p.ks + k) : size_t(s)) * p.b_stage_bytes) >> 4);
           if (TAPS == 9) {
             for (int b = 0; b < p.MB; ++b)
               umma9_i8(d0 + uint32_t(b * p.n_tile), a_s + uint64_t(block_q0(p, b)), b_s, pp, bs, p.idesc);
@@ -609,7 +650,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     __syncwarp();
   } else if (warp == BLOAD_WARP) {
     // ============ weight stages: one bulk copy per stage ============
-    if (lane == 0) {
+    if (lane == 0 && p.b_resident) {  // every weight stage, once
+      const uint32_t total = uint32_t(p.n_tiles * p.ks) * p.b_stage_bytes;
+      mbar_arrive_expect_tx(smem_u32(bres), total);
+      for (uint32_t off = 0; off < total; off += 32768u)
+        bulk_g2s(smem_u32(b_base + off), p.b + off, min(32768u, total - off), smem_u32(bres));
+    } else if (lane == 0) {
       int s = 0, ph = 0, g = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
         const int nt = t % p.n_tiles;
@@ -634,12 +680,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     const int half = warp >> 2;
     const int m = quarter * 32 + lane;
     const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
-    const int f = p.u8_act ? 2 : 1;
     // unit (block b, run ri) belongs to this warp iff its parity matches
     auto mine = [&](int b, int ri) { return ((p.MB >= 2 ? b : ri) & 1) == half; };
     // bias -> TMEM for every (block, run) unit this warp owns in tile t
     auto init_buffer = [&](int t, int ab) {
-      if (t < p.num_tiles) {
+      if (t < p.num_tiles && !p.mma_bias) {
         const int nt = t % p.n_tiles;
         const int jt = nt * p.n_tile;
         for (int ri = 0; ri < 8; ++ri) {
@@ -716,6 +761,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
             }
           } else {
             // trace mode: also recover the reference accumulators
+            const int f = p.u8_act ? 2 : 1;
 #pragma unroll 1
             for (int rr = 0; rr < rn.y; ++rr) {
               uint32_t v[32];
@@ -929,6 +975,48 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
   cv->c_out_pad = c_out_pad;
   cv->n_tile = n_tile;
   cv->n_tiles = n_tiles;
+  // one-tap layers: bias enters the accumulator through an MMA of a ones slab
+  // (16 x 1 and 16 x 127 per row) with a per-N-tile bias slab (s8 column
+  // sum(lo) + 127 * sum(hi) = bias), so the epilogue never initialises TMEM.
+  // Identical slabs (tconv taps repeat the channels) are stored once.
+  cv->n_slabs = 0;
+  if (taps == 1) {
+    std::vector<int8_t> slabs;
+    std::vector<int32_t> slab_of(n_tiles);
+    const size_t sb = size_t(n_tile) * 32;
+    for (int nt = 0; nt < n_tiles; ++nt) {
+      std::vector<int8_t> sl(sb, 0);
+      for (int n = 0; n < n_tile; ++n) {
+        const int bias = col_bias[size_t(nt) * n_tile + n];
+        int hi = (bias >= 0 ? bias + 63 : bias - 63) / 127;
+        const int lo = bias - 127 * hi;
+        sl[size_t(n) * 16] = int8_t(lo);  // khalf 0, k 0
+        for (int i = 0; i < 16; ++i) {     // khalf 1: hi spread over 16 entries
+          const int part = hi / (16 - i);
+          sl[size_t(n_tile) * 16 + size_t(n) * 16 + i] = int8_t(part);
+          hi -= part;
+        }
+      }
+      int found = -1;
+      for (size_t k = 0; k * sb < slabs.size(); ++k)
+        if (std::equal(sl.begin(), sl.end(), slabs.begin() + k * sb)) found = int(k);
+      if (found < 0) {
+        found = int(slabs.size() / sb);
+        slabs.insert(slabs.end(), sl.begin(), sl.end());
+      }
+      slab_of[nt] = found;
+    }
+    if (slabs.size() <= 16384) {
+      MBU_TRY(check_cuda(cudaMalloc(&cv->d_bias_slab, slabs.size()), "alloc bias slabs"));
+      MBU_TRY(check_cuda(cudaMemcpy(cv->d_bias_slab, slabs.data(), slabs.size(), cudaMemcpyHostToDevice),
+                         "upload bias slabs"));
+      MBU_TRY(check_cuda(cudaMalloc(&cv->d_slab_of_nt, n_tiles * sizeof(int32_t)), "alloc slab map"));
+      MBU_TRY(check_cuda(cudaMemcpy(cv->d_slab_of_nt, slab_of.data(), n_tiles * sizeof(int32_t),
+                                    cudaMemcpyHostToDevice),
+                         "upload slab map"));
+      cv->n_slabs = int(slabs.size() / sb);
+    }
+  }
   cv->b_stage_bytes = b_stage;
   cv->tc_ok = 1;
   return MBU_OK;
@@ -945,6 +1033,8 @@ static int num_sms() {
   return sms;
 }
 
+// (a separate trace-free instantiation was tried: ptxas then spills in the
+// epilogue and the N = 64 layers lose ~7%, so trace stays a runtime branch)
 template <int TAPS, bool TCONV, int LA, int CPS>
 static int launch_tc_impl(const tc::Params &p, int grid, size_t smem, cudaStream_t st) {
   static bool configured = false;
@@ -973,7 +1063,7 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   p.halo = cv->taps == 9 ? 1 : 0;
   p.n_tile = cv->n_tile;
   p.n_tiles = cv->n_tiles;
-  p.MB = std::min(8, tc::ACC_COLS / cv->n_tile);
+  p.MB = std::min(cv->taps == 9 ? 8 : 4, tc::ACC_COLS / cv->n_tile);  // one tap: Q <= 512
   if (x.w >= 128) {
     p.row_mode = 1;
     p.TW = 128;
@@ -995,7 +1085,7 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   int Q = q_last + tc::BLOCK_M + (p.halo ? p.P + 1 : 0);
   Q = std::max(Q, (p.R + 2 * p.halo) * p.P);
   Q = (Q + 7) / 8 * 8;
-  if (Q > tc::PROD_ITEMS * tc::PROD_THREADS)
+  if (Q > tc::prod_items(cv->taps) * tc::PROD_THREADS)
     return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv strip taller than the producer tiling");
   p.Q = Q;
   // one-tap convs pack four 32-lane chunks (a 128-lane block) into a stage
@@ -1006,14 +1096,35 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   p.a_chunk_bytes = uint32_t(Q) * 32;
   p.a_stage_bytes = uint32_t((size_t(Q) * 32 * cps + 1023) / 1024 * 1024);
   p.b_stage_bytes = uint32_t(cv->b_stage_bytes * cps);
-  const size_t stage = size_t(p.a_stage_bytes) + p.b_stage_bytes;
   const int raw_stages = (cv->taps == 9 ? tc::LA_CONV3 : tc::LA_TAP1) + 1;
-  // raw-bit ring + per-N-tile run table + per-column biases
-  const size_t raw_bytes = size_t(raw_stages) * Q * cps * 4 + size_t(cv->n_tiles) * 8 * 16 +
-                           size_t(cv->n_tiles) * cv->n_tile * 4;
-  int stages = int((227 * 1024 - tc::SMEM_HEADER - raw_bytes) / stage);
+  // shared memory: [header][A stages][B stages | resident B][raw ring][runs, biases][ones][slabs][slab map]
+  const size_t raw_bytes = size_t(raw_stages) * Q * cps * 4;
+  const size_t runs_bytes = size_t(cv->n_tiles) * 8 * 16 + size_t(cv->n_tiles) * cv->n_tile * 4;
+  const size_t bias_bytes = cv->n_slabs ? 4096 + size_t(cv->n_slabs) * cv->n_tile * 32 + 1024 : 0;
+  const size_t budget = 227 * 1024 - tc::SMEM_HEADER - raw_bytes - runs_bytes - bias_bytes - 1024;
+  const size_t b_all = size_t(cv->n_tiles) * p.ks * p.b_stage_bytes;
+  p.b_resident = b_all + 3 * size_t(p.a_stage_bytes) <= budget;
+  const size_t stage = size_t(p.a_stage_bytes) + (p.b_resident ? 0 : p.b_stage_bytes);
+  int stages = int((budget - (p.b_resident ? b_all : 0)) / stage);
   if (stages < 2) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv stage does not fit in shared memory");
   p.stages = std::min(stages, tc::MAX_STAGES);
+  size_t off = tc::SMEM_HEADER + size_t(p.stages) * p.a_stage_bytes;
+  p.off_b = uint32_t(off);
+  off += p.b_resident ? b_all : size_t(p.stages) * p.b_stage_bytes;
+  p.off_raw = uint32_t(off);
+  off += raw_bytes;
+  p.off_runs = uint32_t(off);
+  off += runs_bytes;
+  p.mma_bias = cv->n_slabs > 0;
+  p.n_slabs = cv->n_slabs;
+  p.bias_slab = cv->d_bias_slab;
+  p.slab_of_nt = cv->d_slab_of_nt;
+  off = (off + 1023) / 1024 * 1024;
+  p.off_ones = uint32_t(off);
+  p.off_slab = uint32_t(off + (p.mma_bias ? 4096 : 0));
+  p.off_slabmap = uint32_t(p.off_slab + (p.mma_bias ? size_t(cv->n_slabs) * cv->n_tile * 32 : 0));
+  off = p.off_slabmap + (p.mma_bias ? size_t(cv->n_tiles) * 4 : 0);
+  const size_t smem_total = off;
   p.u8_act = cv->pad_mode != MBU_PAD_ZERO;
   p.kc = cv->kc;
   p.chunk_word = cv->d_chunk_word;
@@ -1041,8 +1152,8 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   if (tiles > 0x7FFFFFFF) return fail(MBU_ERR_SHAPE, "tcgen05 conv grid too large");
   p.num_tiles = int(tiles);
   const int grid = int(std::min<int64_t>(tiles, num_sms()));
-  size_t smem = tc::SMEM_HEADER + size_t(p.stages) * stage + raw_bytes;
-  smem = std::max<size_t>(smem, tc::MIN_SMEM);
+  const size_t smem = std::max<size_t>(smem_total, tc::MIN_SMEM);
+  if (smem > 227 * 1024) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv shared memory layout overflow");
   if (cv->transposed) return launch_tc_impl<1, true, tc::LA_TAP1, 4>(p, grid, smem, st);
   if (cv->taps == 9) return launch_tc_impl<9, false, tc::LA_CONV3, 1>(p, grid, smem, st);
   return launch_tc_impl<1, false, tc::LA_TAP1, 4>(p, grid, smem, st);

@@ -473,6 +473,8 @@ int mbu_conv_destroy(mbu_conv *cv) {
   cudaFree(cv->d_chunk_word);
   cudaFree(cv->d_b);
   cudaFree(cv->d_thr2);
+  cudaFree(cv->d_bias_slab);
+  cudaFree(cv->d_slab_of_nt);
   delete cv;
   return MBU_OK;
 }

@@ -9,7 +9,7 @@ for lib in "$@"; do
 import json, sys
 d = json.load(open("gpurun_out/ab.json"))
 ks = {k["layer"]: k["ms"] for k in d["kernel_breakdown"]}
-print(f'{sys.argv[1]:28s} value {d["value"]:7.1f}  ' + " ".join(f'{n}={ks[n]:.3f}' for n in ("stem2", "down-C1.b", "up-CT4", "up-CT1", "up-C4.a")))
+print(f'{sys.argv[1]:28s} value {d["value"]:7.1f}  ' + " ".join(f'{n}={v:.3f}' for n, v in ks.items()))
 PY
   done
 done
