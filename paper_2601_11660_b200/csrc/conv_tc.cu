@@ -36,12 +36,12 @@
 // moved by (dy-1)*P + (dx-1) rows of 16 B (K-major, no swizzle: one row is
 // 16 B, so any pixel offset is a legal start). Nine MMAs read one strip.
 //
-// Persistent, warp-specialised (576 threads, one CTA per SM):
+// Persistent, warp-specialised (512 threads, one CTA per SM):
 //   warps 0-7   epilogue: bias -> TMEM, TMEM -> sign bits -> HBM. The two
 //               warps of a TMEM lane quarter split M-blocks (or column runs)
-//   warps 8-15  producers: packed bits -> u8/s8 strips, one stage lookahead
-//   warp 16     one lane issues tcgen05.mma; owns TMEM alloc/dealloc
-//   warp 17     one lane streams pre-arranged weight stages (cp.async.bulk)
+//   warps 8-13  producers: packed bits -> u8/s8 strips, raw words LA stages ahead
+//   warp 14     one lane issues tcgen05.mma; owns TMEM alloc/dealloc
+//   warp 15     one lane streams pre-arranged weight stages (cp.async.bulk)
 // Smem stages cycle through full/empty mbarriers; two TMEM accumulator
 // buffers (2 x 256 columns) let the epilogue of tile i overlap the MMAs of
 // tile i+1.
@@ -58,7 +58,9 @@ namespace tc {
 
 constexpr int BLOCK_M = 128;
 constexpr int NUM_EPI_WARPS = 8;
-constexpr int NUM_PROD_WARPS = 8;
+// 16 warps = 4 per SM sub-partition: each thread may hold 128 registers
+// (18 warps would cap the epilogue at 96 and make it spill)
+constexpr int NUM_PROD_WARPS = 6;
 constexpr int PROD_WARP0 = NUM_EPI_WARPS;
 constexpr int MMA_WARP = PROD_WARP0 + NUM_PROD_WARPS;
 constexpr int BLOAD_WARP = MMA_WARP + 1;
@@ -71,12 +73,11 @@ constexpr int MAX_STAGES = 8;
 constexpr int MAX_CHUNKS = 64;  // 32-lane chunks per pixel (2048 lanes)
 constexpr int SMEM_HEADER = 1024;
 constexpr int MIN_SMEM = 120 * 1024;  // > half an SM: exactly one CTA (and TMEM owner) per SM
-// strip rows per producer thread per stage: Q <= 6*256 for the 3x3 conv, <= 2*256 for one tap
-constexpr int PROD_ITEMS = 6;
-constexpr int prod_items(int taps) { return taps == 9 ? 6 : 2; }
+// strip rows per producer thread per stage: Q <= 8*192 for the 3x3 conv, <= 3*192 for one tap
+constexpr int prod_items(int taps) { return taps == 9 ? 8 : 3; }
 // raw-bit stages in flight per producer thread (template LA): 4 for the 3x3
 // conv (each stage feeds nine taps), 8 for 1x1 / tconv (one tap per stage)
-constexpr int LA_CONV3 = 4, LA_TAP1 = 8;
+constexpr int LA_CONV3 = 8, LA_TAP1 = 8;
 
 struct Params {
   const uint32_t *x32;
@@ -84,6 +85,7 @@ struct Params {
   int x_stride32, x_off32;
   int halo, P, Q, R, TW, row_mode, MB;
   uint32_t p_magic;         // ceil(2^32 / P): q / P == umulhi(q, p_magic) for q < 2^16
+  uint32_t nt_magic, ct_magic, rt_magic;  // same for n_tiles, col_tiles, row_tiles (t < 2^24)
   int col_tiles, row_tiles, n_tiles, num_tiles;
   int u8_act;               // 1: A = bits as u8 {0,1} (neg_one); 0: s8 {-1,0,+1} (zero pad)
   int kc;                   // active 32-lane chunks per pixel
@@ -318,14 +320,22 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
 struct Tile {
   int nb, y0, x0, nt;
 };
+// exact quotient n / d with m = ceil(2^32 / d) when n * d < 2^32 (host-checked);
+// d = 1 is encoded as m = 0
+__device__ __forceinline__ int fdiv(int n, uint32_t m) {
+  return m ? int(__umulhi(uint32_t(n), m)) : n;
+}
 __device__ __forceinline__ Tile decode_tile(const Params &p, int t) {
   Tile r;
-  r.nt = t % p.n_tiles;
-  t /= p.n_tiles;
-  const int ct = t % p.col_tiles;
-  t /= p.col_tiles;
-  const int rt = t % p.row_tiles;
-  r.nb = t / p.row_tiles;
+  int q = fdiv(t, p.nt_magic);
+  r.nt = t - q * p.n_tiles;
+  t = q;
+  q = fdiv(t, p.ct_magic);
+  const int ct = t - q * p.col_tiles;
+  t = q;
+  q = fdiv(t, p.rt_magic);
+  const int rt = t - q * p.row_tiles;
+  r.nb = q;
   r.y0 = rt * p.R;
   r.x0 = ct * p.TW;
   return r;
@@ -612,7 +622,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       int s = 0, ph = 0, it = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         const int ab = it & 1;
-        const int nt = t % p.n_tiles;
+        const int nt = t - fdiv(t, p.nt_magic) * p.n_tiles;
         mbar_wait(smem_u32(&acc_empty[ab]), (it >> 1) & 1);
         tc_fence_after();
         const uint32_t d0 = tmem + uint32_t(ab * ACC_COLS);
@@ -658,7 +668,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     } else if (lane == 0) {
       int s = 0, ph = 0, g = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        const int nt = t % p.n_tiles;
+        const int nt = t - fdiv(t, p.nt_magic) * p.n_tiles;
         const int8_t *src = p.b + size_t(nt) * p.ks * p.b_stage_bytes;
         for (int k = 0; k < p.ks; ++k, ++g) {
           if (g >= S) mbar_wait(smem_u32(&empty[s]), ph ^ 1);
@@ -685,7 +695,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     // bias -> TMEM for every (block, run) unit this warp owns in tile t
     auto init_buffer = [&](int t, int ab) {
       if (t < p.num_tiles && !p.mma_bias) {
-        const int nt = t % p.n_tiles;
+        const int nt = t - fdiv(t, p.nt_magic) * p.n_tiles;
         const int jt = nt * p.n_tile;
         for (int ri = 0; ri < 8; ++ri) {
           const int4 rn = runs_s[nt * 8 + ri];
@@ -760,14 +770,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
               }
             }
           } else {
-            // trace mode: also recover the reference accumulators
+            // trace mode: also recover the reference accumulators; the sign words
+            // go straight to memory (no dynamic index into w8, which must stay
+            // in registers for the fast path)
             const int f = p.u8_act ? 2 : 1;
+            const int g0 = rn.z >> 5;
 #pragma unroll 1
             for (int rr = 0; rr < rn.y; ++rr) {
               uint32_t v[32];
               const int gg = rn.x + rr;
               tmem_ld32(col0 + uint32_t(rr * 32), v);
-              w8[rr] = pack_nonneg<0>(v);
+              const uint32_t word = pack_nonneg<0>(v);
               if (valid) {
                 const int oc = rn.z + 32 * rr;
                 const int jc = jt + 32 * gg;
@@ -779,8 +792,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
                     dst[i] = f * (s * (int(v[i]) - bias)) - __ldg(p.col_w + jc + i);
                   }
                 }
+                if (p.bits) p.bits[opix * p.out_stride32 + p.out_off32 + g0 + rr] = word;
               }
             }
+            if (valid && p.bits && g0 + rn.y == p.c_out_pad / 32)  // pad words of the block
+              for (int i = g0 + rn.y; i < p.out_groups; ++i)
+                p.bits[opix * p.out_stride32 + p.out_off32 + i] = 0u;
+            continue;
           }
           if (valid && p.bits) {
             // write the run; when it ends the pixel's channels append the zero
@@ -833,7 +851,6 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
   const bool tconv = cv->transposed && cv->stride <= 4;
   if (!(conv3 || conv1 || tconv)) return MBU_OK;
   const int lpp = cv->lpp;
-  const int n_chunks = lpp / 32;
   std::vector<uint8_t> real(lpp, 0);
   for (int i = 0; i < n_seg; ++i)
     for (int l = seg_off[i]; l < seg_off[i] + seg_cnt[i]; ++l) real[l] = 1;
@@ -975,12 +992,12 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
   cv->c_out_pad = c_out_pad;
   cv->n_tile = n_tile;
   cv->n_tiles = n_tiles;
-  // one-tap layers: bias enters the accumulator through an MMA of a ones slab
+  // bias enters the accumulator through an MMA of a ones slab
   // (16 x 1 and 16 x 127 per row) with a per-N-tile bias slab (s8 column
   // sum(lo) + 127 * sum(hi) = bias), so the epilogue never initialises TMEM.
   // Identical slabs (tconv taps repeat the channels) are stored once.
   cv->n_slabs = 0;
-  if (taps == 1) {
+  {
     std::vector<int8_t> slabs;
     std::vector<int32_t> slab_of(n_tiles);
     const size_t sb = size_t(n_tile) * 32;
@@ -1151,6 +1168,17 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   if (tiles == 0) return MBU_OK;
   if (tiles > 0x7FFFFFFF) return fail(MBU_ERR_SHAPE, "tcgen05 conv grid too large");
   p.num_tiles = int(tiles);
+  // magic divisors: umulhi(n, ceil(2^32/d)) == n / d whenever n * d < 2^32
+  auto magic = [](int d) { return d == 1 ? 0u : uint32_t((0x100000000ull + d - 1) / d); };
+  {
+    const uint64_t t1 = uint64_t(tiles), t2 = t1 / cv->n_tiles, t3 = t2 / p.col_tiles;
+    if (t1 * cv->n_tiles >= (1ull << 32) || t2 * p.col_tiles >= (1ull << 32) ||
+        t3 * p.row_tiles >= (1ull << 32))
+      return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv tile grid outside the magic-division range");
+  }
+  p.nt_magic = magic(cv->n_tiles);
+  p.ct_magic = magic(p.col_tiles);
+  p.rt_magic = magic(p.row_tiles);
   const int grid = int(std::min<int64_t>(tiles, num_sms()));
   const size_t smem = std::max<size_t>(smem_total, tc::MIN_SMEM);
   if (smem > 227 * 1024) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv shared memory layout overflow");
