@@ -3,6 +3,7 @@
 
     python tools/ncu_summary.py launches gpurun_out/launches.csv > profiles/x_launches.md
     python tools/ncu_summary.py full gpurun_out/prof.ncu-rep [names...] > profiles/x_full.md
+    python tools/ncu_summary.py multi name1=a.ncu-rep name2=b.ncu-rep ... > profiles/x_full.md
 """
 import csv
 import io
@@ -68,8 +69,32 @@ def full(path, names):
             print(f"| {label} (`{key}`) | {units[i]} | " + " | ".join(d[i] for d in data) + " |")
 
 
+def multi(pairs):
+    """One column per report (first launch of each): name=path arguments."""
+    cols, datas, units, idx = [], [], None, None
+    for pr in pairs:
+        name, path = pr.split("=", 1)
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
+        hdr, u, data = rows[0], rows[1], rows[2:]
+        i = {h: k for k, h in enumerate(hdr)}
+        cols.append(name)
+        datas.append({h: data[0][k] for h, k in i.items()})
+        units = units or {h: u[k] for h, k in i.items()}
+    print("# ncu --set full summary (first captured launch of each report)\n")
+    print("| metric | unit | " + " | ".join(cols) + " |")
+    print("|---|---|" + "---|" * len(cols))
+    print("| kernel | | " + " | ".join(f"`{d.get('Kernel Name', '').split('(')[0]}`" for d in datas) + " |")
+    for key, label in KEYS:
+        if key in units:
+            print(f"| {label} (`{key}`) | {units[key]} | " + " | ".join(d.get(key, "") for d in datas) + " |")
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "launches":
+    if sys.argv[1] == "multi":
+        multi(sys.argv[2:])
+    elif sys.argv[1] == "launches":
         launches(sys.argv[2])
     else:
         full(sys.argv[2], sys.argv[3:])
