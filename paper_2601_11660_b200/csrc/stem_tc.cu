@@ -21,12 +21,14 @@
 // c' = 2048*cA + cB + cC = 2^j * s * (bias - A*) (s = sign(gamma); s = -1 also
 // negates the weights; A* is the exact float64 decision point below). TMEM
 // then holds D ~= 2^j * s * (acc - A*) and the bit is D >= 0. The dropped
-// terms are <= 3 * 2^-22 * sum|x||w'| (+ 2^-25 absolute per subnormal part)
-// and the fp32 accumulation of 9 MMAs adds at most ~1.8e-5 of the largest
-// partial sum even if every aligned addend is truncated, so whenever
-//     |D| <= margin_o = eps * (max|x|_tile * sum|w'_o| + |c'_o|) + absolute terms
-// (eps = 3e-5; the filter uses the largest channel margin, the re-check
-// test each channel's own) the epilogue recomputes acc
+// terms are <= 3 * 2^-22 * sum|x||w'| (+ 2^-25 absolute per subnormal part);
+// the fp32 accumulation (exact products, addends aligned to the largest with
+// guard bits and truncated: <= 17 * 2^-26 of the largest term per MMA) adds
+// <= 2.3e-6 over 9 MMAs, ~3.3e-6 in total. Measured on B200 over 3.1 M
+// (pixel, channel) pairs: max |D - D_exact| = 2.7e-7 of the scale below. So
+// whenever
+//     |D| <= margin = eps * (max|x|_tile * sum|w'_o| + |c'_o|) + absolute terms
+// (eps = 8e-6, largest over channels) the epilogue recomputes acc
 // in float64 in the reference's order (fconv_at order, generic.cu) from the
 // tile's raw float64 input, which it still holds in shared memory, and
 // compares it with the exact float64 decision point A*: the reference
@@ -100,7 +102,7 @@ static_assert(OFF_B + CONST_BYTES <= OFF_RAW, "constant block overlaps the raw r
 constexpr uint32_t OFF_A = OFF_RAW + NRAW * RAW_STRIDE;
 constexpr uint32_t SMEM_BYTES = OFF_A + NA * A_STRIDE;
 static_assert(SMEM_BYTES <= 227 * 1024, "stem tile does not fit in shared memory");
-constexpr double EPS = 3e-5;          // relative margin (see above)
+constexpr double EPS = 8e-6;          // relative margin (see above)
 constexpr double ABS_ULP = 2.9802322387695312e-08;  // 2^-25: fp16 subnormal rounding
 
 // per output channel: exact decision point and re-check margin
