@@ -398,19 +398,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
   for (int i = threadIdx.x; i < p.kc; i += blockDim.x) chunk_s[i] = p.chunk_word[i];
   // per-N-tile epilogue runs and per-column TMEM biases, staged once per CTA
   int4 *runs_s = reinterpret_cast<int4 *>(smem + p.off_runs);
-  int32_t *bias_s = reinterpret_cast<int32_t *>(runs_s + p.n_tiles * 8);
+  int32_t *bias_s = reinterpret_cast<int32_t *>(runs_s + p.n_tiles * 9);
   for (int i = threadIdx.x; i < p.n_tiles * p.n_tile; i += blockDim.x) bias_s[i] = p.col_bias[i];
-  if (threadIdx.x < p.n_tiles) {
+  if (threadIdx.x < p.n_tiles) {  // runs_s[nt * 9] = (count), then up to 8 runs
     const int nt = threadIdx.x, groups = p.n_tile / 32;
     int g = 0, r = 0;
     while (g < groups && r < 8) {
       const Run rn = run_at(p, nt * p.n_tile, g, groups, TCONV);
       if (rn.len == 0) break;
       const int dy = TCONV ? rn.tap / p.tconv_s : 0;
-      runs_s[nt * 8 + r++] = make_int4(rn.g, rn.len, rn.o0, (dy << 16) | (rn.tap - dy * p.tconv_s));
+      runs_s[nt * 9 + 1 + r++] = make_int4(rn.g, rn.len, rn.o0, (dy << 16) | (rn.tap - dy * p.tconv_s));
       g += rn.len;
     }
-    for (; r < 8; ++r) runs_s[nt * 8 + r] = make_int4(0, 0, 0, 0);
+    runs_s[nt * 9] = make_int4(r, 0, 0, 0);
   }
   if (p.mma_bias) {  // ones slab (16 x 1, 16 x 127 per row) + bias slabs, read by the tensor core
     uint4 *ones = reinterpret_cast<uint4 *>(smem + p.off_ones);
@@ -690,16 +690,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     const int half = warp >> 2;
     const int m = quarter * 32 + lane;
     const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
-    // unit (block b, run ri) belongs to this warp iff its parity matches
     auto mine = [&](int b, int ri) { return ((p.MB >= 2 ? b : ri) & 1) == half; };
     // bias -> TMEM for every (block, run) unit this warp owns in tile t
     auto init_buffer = [&](int t, int ab) {
       if (t < p.num_tiles && !p.mma_bias) {
         const int nt = t - fdiv(t, p.nt_magic) * p.n_tiles;
         const int jt = nt * p.n_tile;
-        for (int ri = 0; ri < 8; ++ri) {
-          const int4 rn = runs_s[nt * 8 + ri];
-          if (rn.y == 0) break;
+        const int nr = runs_s[nt * 9].x;
+        for (int ri = 0; ri < nr; ++ri) {
+          const int4 rn = runs_s[nt * 9 + 1 + ri];
           for (int b = 0; b < p.MB; ++b) {
             if (!mine(b, ri)) continue;
             for (int gg = rn.x; gg < rn.x + rn.y; ++gg) {
@@ -731,27 +730,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       mbar_wait(smem_u32(&acc_full[ab]), (it >> 1) & 1);
       tc_fence_after();
       const int jt = tl.nt * p.n_tile;
-      for (int ri = 0; ri < 8; ++ri) {
-        const int4 rn = runs_s[tl.nt * 8 + ri];  // (first group, length, o0, tap)
-        if (rn.y == 0) break;
-        for (int b = 0; b < p.MB; ++b) {
-          if (!mine(b, ri)) continue;
-          const int q = block_q0(p, b) + m;
-          const int rq = int(__umulhi(uint32_t(q), p.p_magic));
-          const int r = rq - p.halo;
-          const int c = q - rq * p.P - p.halo;
-          const int yy = tl.y0 + r, xx = tl.x0 + c;
-          const bool valid = r >= 0 && r < p.R && c >= 0 && c < p.TW && yy < p.h && xx < p.w;
-          int oy = yy, ox = xx;
-          if (TCONV) {  // run's tap = (dy, dx) packed as dy << 16 | dx
-            oy = yy * p.tconv_s + (rn.w >> 16);
-            ox = xx * p.tconv_s + (rn.w & 0xFFFF);
-          }
-          const int64_t opix = (int64_t(tl.nb) * p.ho + oy) * p.wo + ox;
+      const int4 *rt = runs_s + tl.nt * 9 + 1;
+      const int nr = runs_s[tl.nt * 9].x;
+      // units (block b, run ri): by block parity when MB >= 2, else by run parity
+      const bool split_b = !TCONV || p.MB >= 2;  // (a conv's N tile <= 128: MB >= 2)
+      for (int b = split_b ? half : 0; b < p.MB; b += split_b ? 2 : 1) {
+        // this lane's pixel in block b, once per block
+        const int q = block_q0(p, b) + m;
+        const int rq = int(__umulhi(uint32_t(q), p.p_magic));
+        const int r = rq - p.halo;
+        const int c = q - rq * p.P - p.halo;
+        const int yy = tl.y0 + r, xx = tl.x0 + c;
+        const bool valid = r >= 0 && r < p.R && c >= 0 && c < p.TW && yy < p.h && xx < p.w;
+        const int64_t pix0 = TCONV ? (int64_t(tl.nb) * p.ho + yy * p.tconv_s) * p.wo + xx * p.tconv_s
+                                   : (int64_t(tl.nb) * p.ho + yy) * p.wo + xx;
+        const uint32_t colb = lane_base + uint32_t(ab * ACC_COLS + b * p.n_tile);
+        for (int ri = split_b ? 0 : half; ri < nr; ri += split_b ? 1 : 2) {
+          const int4 rn = rt[ri];  // (first group, length, o0, tap dy << 16 | dx)
+          const int64_t opix = TCONV ? pix0 + (rn.w >> 16) * p.wo + (rn.w & 0xFFFF) : pix0;
           uint32_t w8[8];
 #pragma unroll
           for (int rr = 0; rr < 8; ++rr) w8[rr] = 0u;
-          const uint32_t col0 = lane_base + uint32_t(ab * ACC_COLS + b * p.n_tile + rn.x * 32);
+          const uint32_t col0 = colb + uint32_t(rn.x * 32);
           if (p.acc == nullptr) {
             // two groups per TMEM load, one SHF per column to pack the signs
 #pragma unroll
@@ -1116,7 +1116,7 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   const int raw_stages = (cv->taps == 9 ? tc::LA_CONV3 : tc::LA_TAP1) + 1;
   // shared memory: [header][A stages][B stages | resident B][raw ring][runs, biases][ones][slabs][slab map]
   const size_t raw_bytes = size_t(raw_stages) * Q * cps * 4;
-  const size_t runs_bytes = size_t(cv->n_tiles) * 8 * 16 + size_t(cv->n_tiles) * cv->n_tile * 4;
+  const size_t runs_bytes = size_t(cv->n_tiles) * 9 * 16 + size_t(cv->n_tiles) * cv->n_tile * 4;
   const size_t bias_bytes = cv->n_slabs ? 4096 + size_t(cv->n_slabs) * cv->n_tile * 32 + 1024 : 0;
   const size_t budget = 227 * 1024 - tc::SMEM_HEADER - raw_bytes - runs_bytes - bias_bytes - 1024;
   const size_t b_all = size_t(cv->n_tiles) * p.ks * p.b_stage_bytes;
