@@ -65,8 +65,10 @@ int mbu_last_path(void);
  * generic kernels instead of the float32-with-exact-recheck stem and the
  * specialised head (results must be identical).
  * MBU_OPT_STEM_FFMA: 1 = run the stem through the float32 CUDA-core kernel
- * instead of the tensor-core (bf16-split) kernel; both recheck in float64. */
-enum { MBU_OPT_GENERIC_ENDPOINTS = 1, MBU_OPT_STEM_FFMA = 2 };
+ * instead of the tensor-core (fp16-split) kernel; both recheck in float64.
+ * MBU_OPT_CONV_I8: 1 = run 3x3 binary convs on kind::i8 instead of kind::mxf4
+ * (e2m1 operands); both are exact integer engines for these operands. */
+enum { MBU_OPT_GENERIC_ENDPOINTS = 1, MBU_OPT_STEM_FFMA = 2, MBU_OPT_CONV_I8 = 3 };
 int mbu_set_option(int option, int value);
 
 /* ------------------------------------------------------------------ */

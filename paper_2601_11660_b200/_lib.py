@@ -79,6 +79,8 @@ def load(path: str | os.PathLike | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if os.environ.get("MBU_CONV_I8"):  # A/B switch for benchmarks: 3x3 convs on kind::i8
+        lib.mbu_set_option(3, 1)
     if path is None:
         _lib = lib
     return lib

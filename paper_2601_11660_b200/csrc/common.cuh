@@ -23,6 +23,7 @@ extern std::atomic<int64_t> g_launches;
 extern int g_last_path;
 extern int g_force_generic_fconv;  // mbu_set_option(MBU_OPT_GENERIC_ENDPOINTS)
 extern int g_force_stem_ffma;      // mbu_set_option(MBU_OPT_STEM_FFMA)
+extern int g_force_conv_i8;        // mbu_set_option(MBU_OPT_CONV_I8)
 
 inline int check_launch(const char *what) {
   cudaError_t e = cudaGetLastError();
@@ -95,7 +96,16 @@ struct mbu_conv {
   int8_t *d_b = nullptr;         // repacked s8 weights, UMMA K-major core-matrix order
   void *d_thr2 = nullptr;        // int2 per GEMM column: bit = (m * acc >= t)
   size_t b_stage_bytes = 0;      // bytes of B per (n tile, 32-lane chunk)
-  int n_slabs = 0;               // one-tap layers: distinct MMA bias slabs (0 = TMEM init)
+  int n_slabs = 0;               // distinct MMA bias slabs (0 = TMEM init)
+  // FP4 (kind::mxf4) operand of 3x3 layers: chunk pairs, e2m1 weights, slabs
+  int fp4_ok = 0;
+  int kp = 0;                    // chunk pairs
+  int pair_consec = 0;           // every pair = two consecutive words, even-aligned
+  int32_t *d_chunk_pair = nullptr;
+  int8_t *d_b4 = nullptr;
+  int n_slabs4 = 0;
+  uint8_t *d_bias_slab4 = nullptr;
+  int32_t *d_slab_of_nt4 = nullptr;
   int8_t *d_bias_slab = nullptr;
   int32_t *d_slab_of_nt = nullptr;
 };
@@ -141,6 +151,8 @@ int head_prepare(mbu_fconv *fc, const double *w, const int32_t *lanes);
 void stem_free(mbu_fconv *fc);
 int stem_tc_prepare(mbu_fconv *fc, const double *w, const double *bias, const double *bn, double eps);
 void stem_tc_free(mbu_fconv *fc);
+bool make_tmap_u32_4d(void *tmap, const void *base, const uint64_t dims[4], const uint64_t strides[3],
+                      const uint32_t box[4]);
 bool stem_tc_usable(const mbu_fconv *fc, const double *x, int w);
 int launch_stem_tc(const mbu_fconv *fc, const double *x, int n, int h, int w, uint64_t *bits,
                    int out_stride, int out_offset, cudaStream_t st);

@@ -45,9 +45,11 @@
 // Smem stages cycle through full/empty mbarriers; two TMEM accumulator
 // buffers (2 x 256 columns) let the epilogue of tile i overlap the MMAs of
 // tile i+1.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -55,6 +57,9 @@
 
 namespace mbu {
 namespace tc {
+#ifdef MBU_TIMELINE
+__device__ unsigned long long g_timeline[64 * 12];
+#endif
 
 constexpr int BLOCK_M = 128;
 constexpr int NUM_EPI_WARPS = 8;
@@ -68,6 +73,7 @@ constexpr int NUM_THREADS = (BLOAD_WARP + 1) * 32;
 constexpr int PROD_THREADS = NUM_PROD_WARPS * 32;
 constexpr int EPI_THREADS = NUM_EPI_WARPS * 32;
 constexpr int ACC_COLS = 256;   // one accumulator buffer
+constexpr int FP4_COLS = 248;   // FP4: the last 8 TMEM columns hold the block scales
 constexpr int TMEM_COLS = 512;  // two buffers
 constexpr int MAX_STAGES = 8;
 constexpr int MAX_CHUNKS = 64;  // 32-lane chunks per pixel (2048 lanes)
@@ -108,6 +114,10 @@ struct Params {
   uint32_t off_b, off_raw, off_runs, off_ones, off_slab, off_slabmap;
   int b_resident;           // all weights resident in smem (loaded once), no B stream
   int mma_bias;             // bias enters the accumulator by an MMA (ones x bias slab)
+  uint32_t sf1, sf256;      // FP4: TMEM columns of the uniform 2^0 / 2^8 block scales
+  // FP4: raw activation blocks arrive by TMA (one box of 16 B x P x strip rows per stage)
+  uint32_t off_rraw, rraw_bytes, rraw_box_bytes;
+  int rraw_stages, raw_rows;
   int n_slabs;
   const int8_t *bias_slab;  // [n_slabs][khalf][n_tile][16]: s8, sum(lo) + 127*sum(hi) = bias
   const int32_t *slab_of_nt;
@@ -223,6 +233,53 @@ __device__ __forceinline__ void umma1_i8(uint32_t tmem_d, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc)
       : "memory");
 }
+// kind::mxf4 (e2m1 operands, UE8M0 block scales read from TMEM): nine taps of
+// one M block, same descriptor walk as umma9_i8
+__device__ __forceinline__ void umma9_fp4(uint32_t tmem_d, uint64_t a_c, uint64_t b0, uint64_t pp,
+                                          uint64_t bs, uint32_t idesc, uint32_t sf) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 am, ap, a, b;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, 1, 0;\n\t"
+      "sub.s64 am, %1, %3;\n\t"
+      "add.s64 ap, %1, %3;\n\t"
+      "add.s64 a, am, -1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, %2, %5, [%6], [%6], p;\n\t"
+      "add.s64 b, %2, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], am, b, %5, [%6], [%6], p;\n\t"
+      "add.s64 a, am, 1;\n\t"
+      "add.s64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %5, [%6], [%6], p;\n\t"
+      "add.s64 a, %1, -1;\n\t"
+      "add.s64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %5, [%6], [%6], p;\n\t"
+      "add.s64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, b, %5, [%6], [%6], p;\n\t"
+      "add.s64 a, %1, 1;\n\t"
+      "add.s64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %5, [%6], [%6], p;\n\t"
+      "add.s64 a, ap, -1;\n\t"
+      "add.s64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %5, [%6], [%6], p;\n\t"
+      "add.s64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], ap, b, %5, [%6], [%6], p;\n\t"
+      "add.s64 a, ap, 1;\n\t"
+      "add.s64 b, b, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %5, [%6], [%6], p;\n\t}" ::"r"(tmem_d),
+      "l"(a_c), "l"(b0), "l"(pp), "l"(bs), "r"(idesc), "r"(sf)
+      : "memory");
+}
+// one kind::mxf4 MMA (bias MMAs): acc = 0 overwrites, separate A / B scale columns
+__device__ __forceinline__ void umma1_fp4(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t sfa, uint32_t sfb, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(sfa), "r"(sfb), "r"(acc)
+      : "memory");
+}
 // overwrite form (accumulate = 0): the bias MMA that opens a tile
 __device__ __forceinline__ void umma1_i8_first(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc) {
   asm volatile(
@@ -317,6 +374,18 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
                : "memory");
 }
 
+// 32 activation bits -> 32 e2m1 lanes (16 B): each 2-bit field picks one byte
+// of `lut` (u8 mode: {0, 1.0}; s8 mode: {-1.0, +1.0}), lane 2j in the low nibble
+__device__ __forceinline__ uint32_t fp4_sel(uint32_t v) {  // byte b of a 16-bit slot -> 4 selector nibbles
+  v = (v & 0x000F000Fu) | ((v << 4) & 0x0F000F00u);
+  return (v & 0x03030303u) | ((v << 2) & 0x30303030u);
+}
+__device__ __forceinline__ uint4 fp4x32(uint32_t w, uint32_t lut) {
+  const uint32_t s0 = fp4_sel(__byte_perm(w, 0u, 0x4140)), s1 = fp4_sel(__byte_perm(w, 0u, 0x4342));
+  return make_uint4(__byte_perm(lut, 0u, s0), __byte_perm(lut, 0u, s0 >> 16), __byte_perm(lut, 0u, s1),
+                    __byte_perm(lut, 0u, s1 >> 16));
+}
+
 struct Tile {
   int nb, y0, x0, nt;
 };
@@ -364,8 +433,9 @@ __device__ __forceinline__ Run run_at(const Params &p, int jt, int g, int groups
 }
 
 // ------------------------------------------------------------------ kernel
-template <int TAPS, bool TCONV, int LA, int CPS>
-__global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_constant__ Params p) {
+template <int TAPS, bool TCONV, int LA, int CPS, bool FP4>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    conv_tc_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap xmap) {
   constexpr int RAW_STAGES = LA + 1;
   constexpr int PI = prod_items(TAPS);
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -374,7 +444,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
   uint64_t *acc_full = empty + MAX_STAGES;
   uint64_t *acc_empty = acc_full + 2;
   uint64_t *bres = acc_empty + 2;  // resident weights landed
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bres + 1);
+  uint64_t *rfull = bres + 1;       // [8] FP4: raw box landed (TMA)
+  uint64_t *rempty = rfull + 8;     // [8] FP4: raw box consumed (producers)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rempty + 8);
   int32_t *chunk_s = reinterpret_cast<int32_t *>(smem + 512);  // MAX_CHUNKS words
   uint8_t *a_base = smem + SMEM_HEADER;
   uint8_t *b_base = smem + p.off_b;
@@ -389,6 +461,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       mbar_init(smem_u32(&empty[s]), 1);
     }
     mbar_init(smem_u32(bres), 1);
+    for (int i = 0; i < 8; ++i) {
+      mbar_init(smem_u32(&rfull[i]), 1);
+      mbar_init(smem_u32(&rempty[i]), PROD_THREADS);
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&acc_full[i]), 1);
       mbar_init(smem_u32(&acc_empty[i]), EPI_THREADS);
@@ -413,13 +489,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     runs_s[nt * 9] = make_int4(r, 0, 0, 0);
   }
   if (p.mma_bias) {  // ones slab (16 x 1, 16 x 127 per row) + bias slabs, read by the tensor core
+    // (FP4: every entry e2m1 1.0; bias = sum(lo) + 256 * sum(hi), two slabs per N tile)
     uint4 *ones = reinterpret_cast<uint4 *>(smem + p.off_ones);
     for (int i = threadIdx.x; i < 256; i += blockDim.x)
-      ones[i] = i < 128 ? make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u)
-                        : make_uint4(0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu);
+      ones[i] = FP4 ? make_uint4(0x22222222u, 0x22222222u, 0x22222222u, 0x22222222u)
+                    : i < 128 ? make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u)
+                              : make_uint4(0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu);
     uint4 *slab = reinterpret_cast<uint4 *>(smem + p.off_slab);
     const uint4 *src = reinterpret_cast<const uint4 *>(p.bias_slab);
-    for (int i = threadIdx.x; i < p.n_slabs * p.n_tile * 2; i += blockDim.x) slab[i] = src[i];
+    for (int i = threadIdx.x; i < p.n_slabs * p.n_tile * (FP4 ? 4 : 2); i += blockDim.x) slab[i] = src[i];
     int32_t *smap = reinterpret_cast<int32_t *>(smem + p.off_slabmap);
     for (int i = threadIdx.x; i < p.n_tiles; i += blockDim.x) smap[i] = p.slab_of_nt[i];
     fence_proxy_async();
@@ -435,6 +513,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if constexpr (FP4) {
+    // uniform block scales: 4 columns of 2^0 and 4 of 2^8 (any scale layout reads one value)
+    if (warp < 4) {
+      const uint32_t lq = tmem + (uint32_t(warp * 32) << 16);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(lq + p.sf1 + c), "r"(0x7F7F7F7Fu)
+                     : "memory");
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(lq + p.sf256 + c), "r"(0x87878787u)
+                     : "memory");
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      asm volatile("bar.sync 1, 160;" ::: "memory");
+    } else if (warp == MMA_WARP) {
+      asm volatile("bar.sync 1, 160;" ::: "memory");
+      tc_fence_after();
+    }
+  }
 
   if (warp >= PROD_WARP0 && warp < MMA_WARP) {
     // ============ producers: packed bits -> u8/s8 strips ============
@@ -532,38 +629,81 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       }
       if (++i_slot == RAW_STAGES) i_slot = 0;
     };
+    int rs = 0, rph = 0;  // FP4: raw box ring (TMA)
+    if constexpr (!FP4) {
 #pragma unroll 1
-    for (int g = 0; g < LA; ++g) issue();
+      for (int g = 0; g < LA; ++g) issue();
+    }
     for (int g = 0; g < n_stages_total; ++g) {
-      issue();
-      asm volatile("cp.async.wait_group %0;" ::"n"(LA) : "memory");  // group g landed
+      if constexpr (!FP4) {
+        issue();
+        asm volatile("cp.async.wait_group %0;" ::"n"(LA) : "memory");  // group g landed
+      } else {
+        mbar_wait(smem_u32(&rfull[rs]), rph);
+      }
       if (e_t != ec.t) tile_offsets(ec, e_t);
-      const uint32_t *rw = raw + e_slot * slot_words;
+      const uint32_t *rw = FP4 ? reinterpret_cast<const uint32_t *>(smem + p.off_rraw + rs * p.rraw_bytes)
+                               : raw + e_slot * slot_words;
+#ifdef MBU_TIMELINE
+      const unsigned long long tp0 = clock64();
+#endif
       if (g >= S) mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+#ifdef MBU_TIMELINE
+      const unsigned long long tp1 = clock64();
+#endif
       const uint32_t a_st = smem_u32(a_base + size_t(s) * p.a_stage_bytes);
-      if constexpr (cps == 1) {
-        const uint32_t a0 = a_st;
-        const uint32_t a1 = a0 + p.Q * 16;
+      // Branch-free expansion (independent rows interleave): out-of-bounds rows
+      // were zero-filled by cp.async, which expands to 0 in u8 mode; s8 mode
+      // masks them explicitly. Indices are clamped so every load is in range.
+      const int qmax = p.Q - 1;
+      if constexpr (FP4) {
+        // two 32-lane chunks -> one K = 64 e2m1 row: chunk c fills core-matrix column c
+        // raw box: 16 B (a 128-lane block) per strip pixel, pixels row-major
+        const uint32_t lut = p.u8_act ? 0x22200200u : 0x222AA2AAu;
+        const int ca = chunk_s[2 * e_k] & 3, cb = chunk_s[2 * e_k + 1] & 3;
+        const int qbox = p.raw_rows * p.P - 1;
 #pragma unroll
         for (int j = 0; j < PI; ++j) {
           const int q = pt + j * PROD_THREADS;
+          const uint32_t *px = rw + min(q, qbox) * 4;
+          const uint32_t lj = ((ec.inb >> j) & 1) ? lut : 0u;  // out of bounds -> 0
+          const uint4 e0 = fp4x32(px[ca], lj), e1 = fp4x32(px[cb], lj);
           if (q < p.Q) {
-            const uint32_t b = rw[q];
-            if ((ec.inb >> j) & 1) {
-              if (p.u8_act) {
-                sts128(a0 + q * 16, spread4(b & 0xF), spread4((b >> 4) & 0xF),
-                       spread4((b >> 8) & 0xF), spread4((b >> 12) & 0xF));
-                sts128(a1 + q * 16, spread4((b >> 16) & 0xF), spread4((b >> 20) & 0xF),
-                       spread4((b >> 24) & 0xF), spread4(b >> 28));
-              } else {
-                sts128(a0 + q * 16, exp4(b & 0xF, 0xFEu, ~0u), exp4((b >> 4) & 0xF, 0xFEu, ~0u),
-                       exp4((b >> 8) & 0xF, 0xFEu, ~0u), exp4((b >> 12) & 0xF, 0xFEu, ~0u));
-                sts128(a1 + q * 16, exp4((b >> 16) & 0xF, 0xFEu, ~0u), exp4((b >> 20) & 0xF, 0xFEu, ~0u),
-                       exp4((b >> 24) & 0xF, 0xFEu, ~0u), exp4(b >> 28, 0xFEu, ~0u));
-              }
-            } else {  // out of bounds: a' = 0, i.e. -1 (u8, neg_one) / a = 0 (s8, zero pad)
-              sts128(a0 + q * 16, 0u, 0u, 0u, 0u);
-              sts128(a1 + q * 16, 0u, 0u, 0u, 0u);
+            const uint32_t a0 = a_st + q * 16;
+            sts128(a0, e0.x, e0.y, e0.z, e0.w);
+            sts128(a0 + p.Q * 16, e1.x, e1.y, e1.z, e1.w);
+          }
+        }
+      } else if constexpr (cps == 1) {
+        const uint32_t a0 = a_st;
+        const uint32_t a1 = a0 + p.Q * 16;
+        if (p.u8_act) {
+#pragma unroll
+          for (int j = 0; j < PI; ++j) {
+            const int q = pt + j * PROD_THREADS;
+            const uint32_t b = rw[min(q, qmax)];
+            const uint32_t v0 = spread4(b & 0xF), v1 = spread4((b >> 4) & 0xF), v2 = spread4((b >> 8) & 0xF),
+                           v3 = spread4((b >> 12) & 0xF), v4 = spread4((b >> 16) & 0xF),
+                           v5 = spread4((b >> 20) & 0xF), v6 = spread4((b >> 24) & 0xF), v7 = spread4(b >> 28);
+            if (q < p.Q) {
+              sts128(a0 + q * 16, v0, v1, v2, v3);
+              sts128(a1 + q * 16, v4, v5, v6, v7);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < PI; ++j) {
+            const int q = pt + j * PROD_THREADS;
+            const uint32_t b = rw[min(q, qmax)];
+            const bool in = (ec.inb >> j) & 1;
+            const uint32_t mul = in ? 0xFEu : 0u, xr = in ? ~0u : 0u;  // a = 0 out of bounds (zero pad)
+            const uint32_t v0 = exp4(b & 0xF, mul, xr), v1 = exp4((b >> 4) & 0xF, mul, xr),
+                           v2 = exp4((b >> 8) & 0xF, mul, xr), v3 = exp4((b >> 12) & 0xF, mul, xr),
+                           v4 = exp4((b >> 16) & 0xF, mul, xr), v5 = exp4((b >> 20) & 0xF, mul, xr),
+                           v6 = exp4((b >> 24) & 0xF, mul, xr), v7 = exp4(b >> 28, mul, xr);
+            if (q < p.Q) {
+              sts128(a0 + q * 16, v0, v1, v2, v3);
+              sts128(a1 + q * 16, v4, v5, v6, v7);
             }
           }
         }
@@ -592,6 +732,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       }
       fence_proxy_async();
       mbar_arrive(smem_u32(&full[s]));
+      if constexpr (FP4) {
+        mbar_arrive(smem_u32(&rempty[rs]));
+        if (++rs == p.rraw_stages) {
+          rs = 0;
+          rph ^= 1;
+        }
+      }
+#ifdef MBU_TIMELINE
+      if (blockIdx.x == 0 && pt == 0 && g < 64) {
+        g_timeline[g * 12 + 8] = tp0;
+        g_timeline[g * 12 + 9] = tp1;
+        g_timeline[g * 12 + 10] = clock64();
+      }
+#endif
       if (++e_k == p.ks) {
         e_k = 0;
         e_t += gridDim.x;
@@ -602,7 +756,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
         ph ^= 1;
       }
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if constexpr (!FP4) asm volatile("cp.async.wait_group 0;" ::: "memory");
   } else if (warp == MMA_WARP) {
     // ============ MMA issue (accumulators pre-loaded with bias) ============
     // The whole warp walks the schedule (all values warp-uniform); one
@@ -623,21 +777,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         const int ab = it & 1;
         const int nt = t - fdiv(t, p.nt_magic) * p.n_tiles;
+#ifdef MBU_TIMELINE
+        unsigned long long tl0 = clock64();
+#endif
         mbar_wait(smem_u32(&acc_empty[ab]), (it >> 1) & 1);
+#ifdef MBU_TIMELINE
+        unsigned long long tl1 = clock64();
+#endif
         tc_fence_after();
         const uint32_t d0 = tmem + uint32_t(ab * ACC_COLS);
-        if (p.mma_bias) {
+        if constexpr (FP4) {  // bias = lo (scale 1) + 256 * hi (A scale 2^8)
+          const uint64_t sd = slab_desc0 + uint64_t(smap[nt]) * uint64_t(p.n_tile * 4);
+          for (int b = 0; b < p.MB; ++b) {
+            umma1_fp4(d0 + uint32_t(b * p.n_tile), ones_desc, sd, p.idesc, tmem + p.sf1, tmem + p.sf1, 0u);
+            umma1_fp4(d0 + uint32_t(b * p.n_tile), ones_desc, sd + uint64_t(p.n_tile * 2), p.idesc,
+                      tmem + p.sf256, tmem + p.sf1, 1u);
+          }
+        } else if (p.mma_bias) {
           const uint64_t sd = slab_desc0 + uint64_t(smap[nt]) * uint64_t(p.n_tile * 2);
           for (int b = 0; b < p.MB; ++b) umma1_i8_first(d0 + uint32_t(b * p.n_tile), ones_desc, sd, p.idesc);
         }
+#ifdef MBU_TIMELINE
+        unsigned long long tl_full = 0;
+#endif
         for (int k = 0; k < p.ks; ++k) {
           mbar_wait(smem_u32(&full[s]), ph);
+#ifdef MBU_TIMELINE
+          if (k == p.ks - 1) tl_full = clock64();
+#endif
           tc_fence_after();
           // descriptors advance by address >> 4 (no carry out of the 14-bit field: smem < 256 KB)
           const uint64_t a_s = a_desc0 + uint64_t((size_t(s) * p.a_stage_bytes) >> 4);
           const uint64_t b_s =
               b_desc0 + uint64_t(((p.b_resident ? size_t(nt * p.ks + k) : size_t(s)) * p.b_stage_bytes) >> 4);
-          if (TAPS == 9) {
+          if constexpr (FP4) {
+            for (int b = 0; b < p.MB; ++b)
+              umma9_fp4(d0 + uint32_t(b * p.n_tile), a_s + uint64_t(block_q0(p, b)), b_s, pp, bs, p.idesc,
+                        tmem + p.sf1);
+          } else if (TAPS == 9) {
             for (int b = 0; b < p.MB; ++b)
               umma9_i8(d0 + uint32_t(b * p.n_tile), a_s + uint64_t(block_q0(p, b)), b_s, pp, bs, p.idesc);
           } else {
@@ -655,6 +832,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
           }
         }
         umma_commit_elect(smem_u32(&acc_full[ab]));
+#ifdef MBU_TIMELINE
+        if (blockIdx.x == 0 && lane == 0 && it < 64) {
+          g_timeline[it * 12 + 0] = tl0;
+          g_timeline[it * 12 + 1] = tl1;
+          g_timeline[it * 12 + 2] = clock64();
+          g_timeline[it * 12 + 3] = tl_full;
+        }
+#endif
       }
     }
     __syncwarp();
@@ -665,20 +850,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       mbar_arrive_expect_tx(smem_u32(bres), total);
       for (uint32_t off = 0; off < total; off += 32768u)
         bulk_g2s(smem_u32(b_base + off), p.b + off, min(32768u, total - off), smem_u32(bres));
-    } else if (lane == 0) {
-      int s = 0, ph = 0, g = 0;
+    }
+    if (lane == 0 && (FP4 || !p.b_resident)) {
+      // per stage: the weight slab (streamed) and, FP4, the raw activation box (TMA)
+      int s = 0, ph = 0, g = 0, rs = 0, rph = 0;
+      if constexpr (FP4) asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        const int nt = t - fdiv(t, p.nt_magic) * p.n_tiles;
-        const int8_t *src = p.b + size_t(nt) * p.ks * p.b_stage_bytes;
+        const Tile tl = decode_tile(p, t);
+        const int8_t *src = p.b + size_t(tl.nt) * p.ks * p.b_stage_bytes;
         for (int k = 0; k < p.ks; ++k, ++g) {
-          if (g >= S) mbar_wait(smem_u32(&empty[s]), ph ^ 1);
-          const uint32_t bar = smem_u32(&full[s]);
-          mbar_arrive_expect_tx(bar, p.b_stage_bytes);
-          bulk_g2s(smem_u32(b_base + size_t(s) * p.b_stage_bytes),
-                   src + size_t(k) * p.b_stage_bytes, p.b_stage_bytes, bar);
-          if (++s == S) {
-            s = 0;
-            ph ^= 1;
+          if constexpr (FP4) {
+            if (g >= p.rraw_stages) mbar_wait(smem_u32(&rempty[rs]), rph ^ 1);
+            const uint32_t rb = smem_u32(&rfull[rs]);
+            mbar_arrive_expect_tx(rb, p.rraw_box_bytes);
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+                "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(smem + p.off_rraw + rs * p.rraw_bytes)),
+                "l"(&xmap), "r"(p.x_off32 + 4 * (chunk_s[2 * k] >> 2)), "r"(tl.x0 - p.halo), "r"(tl.y0 - p.halo),
+                "r"(tl.nb), "r"(rb)
+                : "memory");
+            if (++rs == p.rraw_stages) {
+              rs = 0;
+              rph ^= 1;
+            }
+          }
+          if (!p.b_resident) {
+            if (g >= S) mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+            const uint32_t bar = smem_u32(&full[s]);
+            mbar_arrive_expect_tx(bar, p.b_stage_bytes);
+            bulk_g2s(smem_u32(b_base + size_t(s) * p.b_stage_bytes),
+                     src + size_t(k) * p.b_stage_bytes, p.b_stage_bytes, bar);
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
+            }
           }
         }
       }
@@ -727,7 +932,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
       const int ab = it & 1;
       const Tile tl = decode_tile(p, t);
+#ifdef MBU_TIMELINE
+      unsigned long long te0 = clock64();
+#endif
       mbar_wait(smem_u32(&acc_full[ab]), (it >> 1) & 1);
+#ifdef MBU_TIMELINE
+      unsigned long long te1 = clock64();
+#endif
       tc_fence_after();
       const int jt = tl.nt * p.n_tile;
       const int4 *rt = runs_s + tl.nt * 9 + 1;
@@ -789,7 +1000,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
                 for (int i = 0; i < 32; ++i) {
                   if (oc + i < p.c_out) {
                     const int s = __ldg(p.col_sgn + jc + i), bias = bias_s[jc + i];
-                    dst[i] = f * (s * (int(v[i]) - bias)) - __ldg(p.col_w + jc + i);
+                    // FP4: the accumulator is a float holding D' + 0.5 (never a signed zero)
+                    const int dv = FP4 ? int(__uint_as_float(v[i]) - 0.5f) : int(v[i]);
+                    dst[i] = f * (s * (dv - bias)) - __ldg(p.col_w + jc + i);
                   }
                 }
                 if (p.bits) p.bits[opix * p.out_stride32 + p.out_off32 + g0 + rr] = word;
@@ -822,6 +1035,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc_kernel(const __grid_co
       }
       // buffer drained: re-arm it with the bias of the tile that reuses it
       init_buffer(t + 2 * gridDim.x, ab);
+#ifdef MBU_TIMELINE
+      if (blockIdx.x == 0 && lane == 0 && it < 64 && warp == 0) {
+        g_timeline[it * 12 + 4] = te0;
+        g_timeline[it * 12 + 5] = te1;
+        g_timeline[it * 12 + 6] = clock64();
+      }
+      if (blockIdx.x == 0 && lane == 0 && it < 64 && warp == 4) g_timeline[it * 12 + 7] = clock64();
+#endif
     }
   }
 
@@ -985,6 +1206,106 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
   MBU_TRY(check_cuda(cudaMalloc(&cv->d_thr2, cols.size() * sizeof(int32_t)), "alloc column bias"));
   MBU_TRY(check_cuda(cudaMemcpy(cv->d_thr2, cols.data(), cols.size() * sizeof(int32_t), cudaMemcpyHostToDevice),
                      "upload column bias"));
+  // FP4 (kind::mxf4) operand for 3x3 layers: chunk pairs share one K = 64
+  // row (pair p = chunks 2p, 2p+1; an odd count gets a zero-weight dummy),
+  // weights as e2m1 {-1, 0, +1} nibbles, lane 2i in the low nibble
+  cv->fp4_ok = 0;
+  if (conv3) {
+    // pairs never straddle a 128-lane block (one TMA box per stage): pair the
+    // chunks of each block, an odd leftover with a zero-weight duplicate
+    std::vector<int32_t> pairs, pair_src;  // pair_src: index into chunk_word, or -1 (dummy)
+    for (int i = 0; i < kc;) {
+      const int blk = chunk_word[i] >> 2;
+      pairs.push_back(chunk_word[i]);
+      pair_src.push_back(i);
+      if (i + 1 < kc && (chunk_word[i + 1] >> 2) == blk) {
+        pairs.push_back(chunk_word[i + 1]);
+        pair_src.push_back(i + 1);
+        i += 2;
+      } else {
+        pairs.push_back(chunk_word[i]);
+        pair_src.push_back(-1);
+        i += 1;
+      }
+    }
+    const int kp = int(pairs.size() / 2);
+    bool consec = true;
+    for (int q = 0; q < kp; ++q) consec &= pairs[2 * q] % 2 == 0 && pairs[2 * q + 1] == pairs[2 * q] + 1;
+    std::vector<uint8_t> b4(size_t(n_tiles) * kp * b_stage, 0);
+    auto e2m1 = [](int v) -> uint8_t { return v > 0 ? 0x2 : v < 0 ? 0xA : 0x0; };
+    for (int nt = 0; nt < n_tiles; ++nt)
+      for (int q = 0; q < kp; ++q)
+        for (int tap = 0; tap < taps; ++tap)
+          for (int half = 0; half < 2; ++half)
+            for (int n = 0; n < n_tile; ++n) {
+              const int j = nt * n_tile + n;
+              const int ci = pair_src[2 * q + half];
+              uint8_t *dst = &b4[((size_t(nt) * kp + q) * taps + tap) * n_tile * 32 + size_t(half) * n_tile * 16 +
+                                 size_t(n) * 16];
+              if (ci < 0) continue;  // dummy chunk: zero weights
+              for (int i = 0; i < 32; ++i) {
+                const int v = wval(j, tap, 32 * chunk_word[ci] + i);
+                dst[i / 2] |= uint8_t(e2m1(col_neg[j] ? -v : v) << (4 * (i & 1)));
+              }
+            }
+    // bias slabs: bias + 0.5 (no signed zero) = sum(lo entries) + 256 * sum(hi entries)
+    const size_t sb = size_t(n_tile) * 64;  // lo + hi slabs of one N tile
+    std::vector<uint8_t> slabs;
+    std::vector<int32_t> slab_of(n_tiles);
+    bool slabs_ok = true;
+    for (int nt = 0; nt < n_tiles; ++nt) {
+      std::vector<uint8_t> sl(sb, 0);
+      for (int n = 0; n < n_tile; ++n) {
+        const int bias = col_bias[size_t(nt) * n_tile + n];
+        const int hi = (bias >= 0 ? bias + 128 : bias - 128) / 256;
+        const double lo = double(bias - 256 * hi) + 0.5;
+        for (int part = 0; part < 2; ++part) {
+          const double v = part == 0 ? lo : double(hi);
+          // entries e = 0..63 of column n: khalf e / 32, byte (e % 32) / 2, nibble e % 2
+          static const double mag[7] = {6, 4, 3, 2, 1.5, 1, 0.5};
+          static const uint8_t code[7] = {7, 6, 5, 4, 3, 2, 1};
+          const uint8_t sg = v < 0 ? 0x8 : 0x0;
+          double r = std::fabs(v);
+          int e = 0;
+          for (int m = 0; m < 7; ++m)
+            while (r >= mag[m] && e < 64) {
+              uint8_t *slab = sl.data() + size_t(part) * n_tile * 32;
+              slab[size_t(e / 32) * n_tile * 16 + size_t(n) * 16 + (e % 32) / 2] |=
+                  uint8_t((code[m] | sg) << (4 * (e & 1)));
+              r -= mag[m];
+              ++e;
+            }
+          slabs_ok &= r == 0.0;
+        }
+      }
+      int found = -1;
+      for (size_t k = 0; k * sb < slabs.size(); ++k)
+        if (std::equal(sl.begin(), sl.end(), slabs.begin() + k * sb)) found = int(k);
+      if (found < 0) {
+        found = int(slabs.size() / sb);
+        slabs.insert(slabs.end(), sl.begin(), sl.end());
+      }
+      slab_of[nt] = found;
+    }
+    if (slabs_ok && slabs.size() <= 16384) {
+      MBU_TRY(check_cuda(cudaMalloc(&cv->d_b4, b4.size()), "alloc fp4 weights"));
+      MBU_TRY(check_cuda(cudaMemcpy(cv->d_b4, b4.data(), b4.size(), cudaMemcpyHostToDevice), "upload fp4 weights"));
+      MBU_TRY(check_cuda(cudaMalloc(&cv->d_chunk_pair, pairs.size() * 4), "alloc chunk pairs"));
+      MBU_TRY(check_cuda(cudaMemcpy(cv->d_chunk_pair, pairs.data(), pairs.size() * 4, cudaMemcpyHostToDevice),
+                         "upload chunk pairs"));
+      MBU_TRY(check_cuda(cudaMalloc(&cv->d_bias_slab4, slabs.size()), "alloc fp4 bias slabs"));
+      MBU_TRY(check_cuda(cudaMemcpy(cv->d_bias_slab4, slabs.data(), slabs.size(), cudaMemcpyHostToDevice),
+                         "upload fp4 bias slabs"));
+      MBU_TRY(check_cuda(cudaMalloc(&cv->d_slab_of_nt4, n_tiles * sizeof(int32_t)), "alloc fp4 slab map"));
+      MBU_TRY(check_cuda(cudaMemcpy(cv->d_slab_of_nt4, slab_of.data(), n_tiles * sizeof(int32_t),
+                                    cudaMemcpyHostToDevice),
+                         "upload fp4 slab map"));
+      cv->n_slabs4 = int(slabs.size() / sb);
+      cv->kp = kp;
+      cv->pair_consec = consec ? 1 : 0;
+      cv->fp4_ok = 1;
+    }
+  }
   cv->taps = taps;
   cv->kc = kc;
   cv->n_gemm = n_gemm;
@@ -1052,16 +1373,32 @@ static int num_sms() {
 
 // (a separate trace-free instantiation was tried: ptxas then spills in the
 // epilogue and the N = 64 layers lose ~7%, so trace stays a runtime branch)
-template <int TAPS, bool TCONV, int LA, int CPS>
-static int launch_tc_impl(const tc::Params &p, int grid, size_t smem, cudaStream_t st) {
+template <int TAPS, bool TCONV, int LA, int CPS, bool FP4>
+static int launch_tc_impl(const tc::Params &p, const CUtensorMap &xmap, int grid, size_t smem, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    MBU_TRY(check_cuda(cudaFuncSetAttribute(tc::conv_tc_kernel<TAPS, TCONV, LA, CPS>,
+    MBU_TRY(check_cuda(cudaFuncSetAttribute(tc::conv_tc_kernel<TAPS, TCONV, LA, CPS, FP4>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
                        "cudaFuncSetAttribute"));
     configured = true;
   }
-  tc::conv_tc_kernel<TAPS, TCONV, LA, CPS><<<grid, tc::NUM_THREADS, smem, st>>>(p);
+  tc::conv_tc_kernel<TAPS, TCONV, LA, CPS, FP4><<<grid, tc::NUM_THREADS, smem, st>>>(p, xmap);
+#ifdef MBU_TIMELINE
+  {
+    static int call = 0;
+    unsigned long long h[64 * 12];
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(h, tc::g_timeline, sizeof(h));
+    const unsigned long long b0 = h[0];
+    fprintf(stderr, "TIMELINE call %d taps %d fp4 %d MB %d ntile %d ks %d\n", call++, TAPS, int(FP4), p.MB, p.n_tile, p.ks);
+    for (int i = 0; i < 24; ++i)
+      fprintf(stderr, "  it %2d mma: waitE %6lld got %6lld fullL %6lld issued %6lld | epi0: wait %6lld got %6lld done %6lld | epi4 done %6lld | prod stage %2d: start %6lld emptyok %6lld end %6lld\n", i,
+              (long long)(h[i * 12] - b0), (long long)(h[i * 12 + 1] - b0), (long long)(h[i * 12 + 3] - b0),
+              (long long)(h[i * 12 + 2] - b0), (long long)(h[i * 12 + 4] - b0), (long long)(h[i * 12 + 5] - b0),
+              (long long)(h[i * 12 + 6] - b0), (long long)(h[i * 12 + 7] - b0), i, (long long)(h[i * 12 + 8] - b0),
+              (long long)(h[i * 12 + 9] - b0), (long long)(h[i * 12 + 10] - b0));
+  }
+#endif
   return check_launch("conv_tc_kernel");
 }
 
@@ -1080,7 +1417,11 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   p.halo = cv->taps == 9 ? 1 : 0;
   p.n_tile = cv->n_tile;
   p.n_tiles = cv->n_tiles;
-  p.MB = std::min(cv->taps == 9 ? 8 : 4, tc::ACC_COLS / cv->n_tile);  // one tap: Q <= 512
+  // 3x3 layers run kind::mxf4 (e2m1) when the uniform block-scale columns fit
+  // next to the accumulators (MB * n_tile <= 248); MBU_OPT_CONV_I8 forces kind::i8
+  const bool fp4 = cv->fp4_ok && !g_force_conv_i8 && tc::FP4_COLS / cv->n_tile >= 1;
+  p.MB = fp4 ? std::min(8, tc::FP4_COLS / cv->n_tile)
+             : std::min(cv->taps == 9 ? 8 : 4, tc::ACC_COLS / cv->n_tile);  // one tap: Q <= 512
   if (x.w >= 128) {
     p.row_mode = 1;
     p.TW = 128;
@@ -1105,20 +1446,41 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   if (Q > tc::prod_items(cv->taps) * tc::PROD_THREADS)
     return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv strip taller than the producer tiling");
   p.Q = Q;
-  // one-tap convs pack four 32-lane chunks (a 128-lane block) into a stage
-  const int cps = cv->taps == 1 ? 4 : 1;
-  if (cv->kc % cps) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 one-tap conv needs whole 128-lane blocks");
-  p.ks = cv->kc / cps;
-  p.vec = ((cv->chunk_consec >> (cps >> 1)) & 1) && p.x_stride32 % cps == 0 && p.x_off32 % cps == 0;
+  // one-tap convs pack four 32-lane chunks (a 128-lane block) into a stage;
+  // FP4 3x3 stages hold a chunk pair (K = 64 e2m1 lanes in the same 32 B row)
+  const int cps = fp4 ? 2 : cv->taps == 1 ? 4 : 1;
+  const int kcs = fp4 ? 2 * cv->kp : cv->kc;
+  if (kcs % cps) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 one-tap conv needs whole 128-lane blocks");
+  p.ks = kcs / cps;
+  p.vec = fp4 ? (cv->pair_consec && p.x_stride32 % 2 == 0 && p.x_off32 % 2 == 0)
+              : ((cv->chunk_consec >> (cps >> 1)) & 1) && p.x_stride32 % cps == 0 && p.x_off32 % cps == 0;
   p.a_chunk_bytes = uint32_t(Q) * 32;
-  p.a_stage_bytes = uint32_t((size_t(Q) * 32 * cps + 1023) / 1024 * 1024);
-  p.b_stage_bytes = uint32_t(cv->b_stage_bytes * cps);
+  p.a_stage_bytes = uint32_t((size_t(Q) * 32 * (fp4 ? 1 : cps) + 1023) / 1024 * 1024);
+  p.b_stage_bytes = uint32_t(cv->b_stage_bytes * (fp4 ? 1 : cps));
   const int raw_stages = (cv->taps == 9 ? tc::LA_CONV3 : tc::LA_TAP1) + 1;
   // shared memory: [header][A stages][B stages | resident B][raw ring][runs, biases][ones][slabs][slab map]
-  const size_t raw_bytes = size_t(raw_stages) * Q * cps * 4;
+  // (FP4: the raw ring holds TMA boxes of one 128-lane block per strip pixel)
+  CUtensorMap xmap;
+  std::memset(&xmap, 0, sizeof(xmap));
+  p.raw_rows = p.R + 2 * p.halo;
+  if (fp4) {
+    p.rraw_box_bytes = uint32_t(16) * p.P * p.raw_rows;
+    p.rraw_bytes = (p.rraw_box_bytes + 127) / 128 * 128;
+    p.rraw_stages = 4;
+    const uint64_t dims[4] = {uint64_t(p.x_stride32), uint64_t(x.w), uint64_t(x.h), uint64_t(x.n)};
+    const uint64_t strides[3] = {uint64_t(p.x_stride32) * 4, uint64_t(p.x_stride32) * 4 * x.w,
+                                 uint64_t(p.x_stride32) * 4 * x.w * x.h};
+    const uint32_t box[4] = {4, uint32_t(p.P), uint32_t(p.raw_rows), 1};
+    if (p.P > 256 || p.raw_rows > 256 || p.x_stride32 % 4 || p.x_off32 % 4 ||
+        (reinterpret_cast<uintptr_t>(x.base) & 15) || !make_tmap_u32_4d(&xmap, x.base, dims, strides, box))
+      return fail(MBU_ERR_UNSUPPORTED, "tcgen05 FP4 conv: raw activation tensor map unavailable");
+  }
+  const size_t raw_bytes = fp4 ? size_t(p.rraw_stages) * p.rraw_bytes : size_t(raw_stages) * Q * cps * 4;
   const size_t runs_bytes = size_t(cv->n_tiles) * 9 * 16 + size_t(cv->n_tiles) * cv->n_tile * 4;
-  const size_t bias_bytes = cv->n_slabs ? 4096 + size_t(cv->n_slabs) * cv->n_tile * 32 + 1024 : 0;
-  const size_t budget = 227 * 1024 - tc::SMEM_HEADER - raw_bytes - runs_bytes - bias_bytes - 1024;
+  const int n_slabs = fp4 ? cv->n_slabs4 : cv->n_slabs;
+  const size_t slab_bytes = size_t(n_slabs) * cv->n_tile * (fp4 ? 64 : 32);
+  const size_t bias_bytes = n_slabs ? 4096 + slab_bytes + 1024 : 0;
+  const size_t budget = 227 * 1024 - tc::SMEM_HEADER - raw_bytes - runs_bytes - bias_bytes - 1024 - 128;
   const size_t b_all = size_t(cv->n_tiles) * p.ks * p.b_stage_bytes;
   p.b_resident = b_all + 3 * size_t(p.a_stage_bytes) <= budget;
   const size_t stage = size_t(p.a_stage_bytes) + (p.b_resident ? 0 : p.b_stage_bytes);
@@ -1128,28 +1490,34 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   size_t off = tc::SMEM_HEADER + size_t(p.stages) * p.a_stage_bytes;
   p.off_b = uint32_t(off);
   off += p.b_resident ? b_all : size_t(p.stages) * p.b_stage_bytes;
+  off = (off + 127) / 128 * 128;  // (TMA destinations: 128-B aligned)
   p.off_raw = uint32_t(off);
+  p.off_rraw = uint32_t(off);
   off += raw_bytes;
   p.off_runs = uint32_t(off);
   off += runs_bytes;
-  p.mma_bias = cv->n_slabs > 0;
-  p.n_slabs = cv->n_slabs;
-  p.bias_slab = cv->d_bias_slab;
-  p.slab_of_nt = cv->d_slab_of_nt;
+  p.mma_bias = n_slabs > 0;
+  p.n_slabs = n_slabs;
+  p.bias_slab = fp4 ? reinterpret_cast<const int8_t *>(cv->d_bias_slab4) : cv->d_bias_slab;
+  p.slab_of_nt = fp4 ? cv->d_slab_of_nt4 : cv->d_slab_of_nt;
   off = (off + 1023) / 1024 * 1024;
   p.off_ones = uint32_t(off);
   p.off_slab = uint32_t(off + (p.mma_bias ? 4096 : 0));
-  p.off_slabmap = uint32_t(p.off_slab + (p.mma_bias ? size_t(cv->n_slabs) * cv->n_tile * 32 : 0));
+  p.off_slabmap = uint32_t(p.off_slab + (p.mma_bias ? slab_bytes : 0));
   off = p.off_slabmap + (p.mma_bias ? size_t(cv->n_tiles) * 4 : 0);
   const size_t smem_total = off;
   p.u8_act = cv->pad_mode != MBU_PAD_ZERO;
-  p.kc = cv->kc;
-  p.chunk_word = cv->d_chunk_word;
-  p.b = cv->d_b;
+  p.kc = kcs;
+  p.chunk_word = fp4 ? cv->d_chunk_pair : cv->d_chunk_word;
+  p.b = fp4 ? cv->d_b4 : cv->d_b;
   // instruction descriptor: s32 accum, A u8 (neg_one) / s8 (zero pad), B s8,
-  // K-major both, N, M = 128
-  p.idesc = (2u << 4) | (uint32_t(p.u8_act ? 0 : 1) << 7) | (1u << 10) |
-            (uint32_t(cv->n_tile >> 3) << 17) | (uint32_t(tc::BLOCK_M >> 4) << 24);
+  // K-major both, N, M = 128; FP4: block-scaled, A/B e2m1, UE8M0 scales, K = 64
+  p.idesc = fp4 ? ((1u << 7) | (1u << 10) | (uint32_t(cv->n_tile >> 3) << 17) | (1u << 23) |
+                   (uint32_t(tc::BLOCK_M >> 4) << 24))
+                : ((2u << 4) | (uint32_t(p.u8_act ? 0 : 1) << 7) | (1u << 10) |
+                   (uint32_t(cv->n_tile >> 3) << 17) | (uint32_t(tc::BLOCK_M >> 4) << 24));
+  p.sf1 = tc::TMEM_COLS - 8;
+  p.sf256 = tc::TMEM_COLS - 4;
   p.c_out = cv->c_out;
   p.c_out_pad = cv->c_out_pad;
   p.n_gemm = cv->n_gemm;
@@ -1182,9 +1550,10 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   const int grid = int(std::min<int64_t>(tiles, num_sms()));
   const size_t smem = std::max<size_t>(smem_total, tc::MIN_SMEM);
   if (smem > 227 * 1024) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv shared memory layout overflow");
-  if (cv->transposed) return launch_tc_impl<1, true, tc::LA_TAP1, 4>(p, grid, smem, st);
-  if (cv->taps == 9) return launch_tc_impl<9, false, tc::LA_CONV3, 1>(p, grid, smem, st);
-  return launch_tc_impl<1, false, tc::LA_TAP1, 4>(p, grid, smem, st);
+  if (cv->transposed) return launch_tc_impl<1, true, tc::LA_TAP1, 4, false>(p, xmap, grid, smem, st);
+  if (fp4) return launch_tc_impl<9, false, tc::LA_CONV3, 2, true>(p, xmap, grid, smem, st);
+  if (cv->taps == 9) return launch_tc_impl<9, false, tc::LA_CONV3, 1, false>(p, xmap, grid, smem, st);
+  return launch_tc_impl<1, false, tc::LA_TAP1, 4, false>(p, xmap, grid, smem, st);
 }
 
 }  // namespace mbu

@@ -27,6 +27,7 @@ std::atomic<int64_t> g_launches{0};
 int g_last_path = 0;
 int g_force_generic_fconv = 0;
 int g_force_stem_ffma = 0;
+int g_force_conv_i8 = 0;
 
 void set_error(const std::string &msg) { t_last_error = msg; }
 int fail(int status, const std::string &msg) {
@@ -380,6 +381,10 @@ int mbu_set_option(int option, int value) {
     g_force_stem_ffma = value != 0;
     return MBU_OK;
   }
+  if (option == MBU_OPT_CONV_I8) {
+    g_force_conv_i8 = value != 0;
+    return MBU_OK;
+  }
   return fail(MBU_ERR_ENGINE, "unknown option " + std::to_string(option));
 }
 
@@ -474,6 +479,10 @@ int mbu_conv_destroy(mbu_conv *cv) {
   cudaFree(cv->d_b);
   cudaFree(cv->d_thr2);
   cudaFree(cv->d_bias_slab);
+  cudaFree(cv->d_b4);
+  cudaFree(cv->d_chunk_pair);
+  cudaFree(cv->d_bias_slab4);
+  cudaFree(cv->d_slab_of_nt4);
   cudaFree(cv->d_slab_of_nt);
   delete cv;
   return MBU_OK;

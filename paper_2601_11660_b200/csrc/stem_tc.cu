@@ -707,6 +707,19 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// 4-D u32 tiled tensor map (conv_tc.cu's raw activation boxes)
+bool make_tmap_u32_4d(void *tmap, const void *base, const uint64_t dims[4], const uint64_t strides[3],
+                      const uint32_t box[4]) {
+  if (!encode_fn()) return false;
+  const cuuint64_t d[4] = {dims[0], dims[1], dims[2], dims[3]};
+  const cuuint64_t st[3] = {strides[0], strides[1], strides[2]};
+  const cuuint32_t bx[4] = {box[0], box[1], box[2], box[3]};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return encode_fn()(static_cast<CUtensorMap *>(tmap), CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<void *>(base),
+                     d, st, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool stem_tc_usable(const mbu_fconv *fc, const double *x, int w) {
   return fc->stem_tc && (w % 2) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && encode_fn();
 }

@@ -48,3 +48,16 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.fail("GPU test ran without a CUDA device")
     return torch.device("cuda", 0)
+
+
+@pytest.fixture(params=["fp4", "i8"])
+def conv_engine(request):
+    """Run the test once per tcgen05 operand kind of the 3x3 convs: kind::mxf4
+    (e2m1, default) and kind::i8 (MBU_OPT_CONV_I8)."""
+    from paper_2601_11660_b200 import _lib
+
+    _lib.call("mbu_set_option", 3, 1 if request.param == "i8" else 0)
+    try:
+        yield request.param
+    finally:
+        _lib.call("mbu_set_option", 3, 0)

@@ -37,7 +37,7 @@ def sha(a) -> str:
 
 @pytest.mark.parametrize("variant", sorted(VARIANTS))
 @pytest.mark.parametrize("path", [_lib.PATH_AUTO, _lib.PATH_POPCOUNT])
-def test_tiny_forward_matches_reference_trace(cuda, variant, path):
+def test_tiny_forward_matches_reference_trace(cuda, variant, path, conv_engine):
     z = load_golden("forward_tiny.npz")
     for extent in (16, 32):
         key = f"{variant}@{extent}"
@@ -136,7 +136,7 @@ def test_engine_graph_replay_and_batch_split_at_config3_shape(cuda):
     assert 0.02 < m < 0.98, m  # live generator: a non-trivial mask
 
 
-def test_path_invariance_at_256(cuda):
+def test_path_invariance_at_256(cuda, conv_engine):
     cfg, bundle, model, image = golden_model_256("live", 1)
     a = mb.runtime.forward(model, image, path=_lib.PATH_AUTO)
     b = mb.runtime.forward(model, image, path=_lib.PATH_POPCOUNT)

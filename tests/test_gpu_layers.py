@@ -22,7 +22,7 @@ PATHS = [_lib.PATH_AUTO, _lib.PATH_POPCOUNT]
 
 
 @pytest.mark.parametrize("path", PATHS)
-def test_conv_golden(cuda, path):
+def test_conv_golden(cuda, path, conv_engine):
     z, cases = golden_cases()
     for c in cases:
         k = c["key"]
@@ -70,7 +70,7 @@ def test_pool_and_threshold_golden(cuda):
             assert np.array_equal(got.words, z[f"{k}_out"]), k
 
 
-def test_criterion3_random_layers_vs_oracle(cuda, rng):
+def test_criterion3_random_layers_vs_oracle(cuda, rng, conv_engine):
     """Reference acceptance criterion 3 (test_acceptance.py:183-242), reduced."""
     pool = [64, 128, 192, 256]
     geoms = [(1, 1, 0), (2, 2, 0), (3, 1, 1), (3, 2, 1)]
@@ -91,7 +91,7 @@ def test_criterion3_random_layers_vs_oracle(cuda, rng):
 
 
 @pytest.mark.parametrize("sparsity", [0.5, 0.9, 0.95])
-def test_config2_conv_256_128x128(cuda, sparsity):
+def test_config2_conv_256_128x128(cuda, sparsity, conv_engine):
     """BASELINE config 2: one masked 3x3 conv 256->256 at 128x128, exact."""
     rng = np.random.default_rng(0)
     x = (rng.integers(0, 2, (1, 128, 128, 256)) * 2 - 1).astype(np.int8)
@@ -106,7 +106,7 @@ def test_config2_conv_256_128x128(cuda, sparsity):
     assert np.array_equal(got, ref)
 
 
-def test_odd_channels_and_widths(cuda, rng):
+def test_odd_channels_and_widths(cuda, rng, conv_engine):
     # partial 32-lane chunks, c_out not a multiple of 32, widths not multiples of 128
     for c_in, c_out, h, w in [(70, 9, 5, 7), (33, 40, 3, 130), (112, 64, 9, 33), (1, 1, 2, 2)]:
         x = rng.choice((-1, 1), size=(2, h, w, c_in)).astype(np.int8)

@@ -1,0 +1,165 @@
+// Probe: tcgen05.mma kind::mxf4 (e2m1 operands, UE8M0 scale = 1 everywhere) as an exact
+// integer engine for {-1,0,+1} x {0,1}/{-1,+1} dot products, and its throughput vs N.
+//   - A: 128 rows x 64 e2m1 (32 B per row, K-major, no swizzle), B: N rows x 64 e2m1
+//   - scale factors: TMEM columns 480..511 filled with 0x7F7F7F7F (2^0) -> any layout reads 1.0
+//   - correctness: D after `reps` accumulating MMAs vs the CPU integer result
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/ubench_fp4 tools/ubench_fp4.cu
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = uint64_t((saddr >> 4) & 0x3FFFu);
+  d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
+  d |= uint64_t(1) << 46;
+  return d;
+}
+
+// a: [128][32 B] row-major packed e2m1 (element k of row r in byte r*32 + k/2, nibble k%2)
+// b: [N][32 B]; out: [128][N] floats
+__global__ void fp4_mma(const uint8_t *a, const uint8_t *b, int n, int reps, int timing, float *out,
+                        unsigned long long *clk, int sfc, uint32_t sfa_val) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // core-matrix layout [khalf][row][16 B]
+  for (int i = threadIdx.x; i < 128 * 32; i += blockDim.x) {
+    const int r = i / 32, byte = i % 32, kh = byte / 16;
+    smem[kh * 128 * 16 + r * 16 + (byte % 16)] = a[i];
+  }
+  for (int i = threadIdx.x; i < n * 32; i += blockDim.x) {
+    const int r = i / 32, byte = i % 32, kh = byte / 16;
+    smem[8192 + kh * n * 16 + r * 16 + (byte % 16)] = b[i];
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = slot;
+  // scale factors = 1.0 in columns 480..511 of every lane
+  {
+    const uint32_t base = tmem + (uint32_t(warp * 32) << 16) + 480;
+    for (int c = 0; c < 32; ++c) {
+      uint32_t v = c < sfc ? 0x7F7F7F7Fu : (c >= 16 && c < 16 + sfc ? sfa_val : 0u);
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(base + c), "r"(v) : "memory");
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (threadIdx.x == 0) {
+    const uint64_t ad = umma_desc(smem_u32(smem), 128 * 16, 128);
+    const uint64_t bd = umma_desc(smem_u32(smem + 8192), uint32_t(n) * 16, 128);
+    // block-scaled descriptor: A/B E2M1 (1), UE8M0 scales (bit 23), N, M = 128, K = 64
+    const uint32_t idesc = (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (1u << 23) | (uint32_t(128 >> 4) << 24);
+    const uint32_t sf = tmem + 480;
+    const unsigned long long t0 = clock64();
+    for (int i = 0; i < reps; ++i) {
+      const uint32_t d = tmem;
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+          "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d),
+          "l"(ad), "l"(bd), "r"(idesc), "r"(i > 0 ? 1 : 0), "r"(sf + (sfa_val ? 16u : 0u)), "r"(sf));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{\n\t.reg .pred q;\n\tmbarrier.try_wait.parity.shared::cta.b64 q, [%1], 0;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+                   : "=r"(ok) : "r"(smem_u32(&bar)));
+    clk[blockIdx.x] = clock64() - t0;
+  }
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (!timing && blockIdx.x == 0 && warp < 4) {
+    for (int c = 0; c < n; ++c) {
+      uint32_t v;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(tmem + (uint32_t(warp * 32) << 16) + c));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      out[(warp * 32 + lane) * n + c] = __uint_as_float(v);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(slot));
+}
+
+static uint8_t enc(int v) { return v == 0 ? 0x0 : v == 1 ? 0x2 : v == -1 ? 0xA : v == 6 ? 0x7 : 0xF; }
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaFuncSetAttribute(fp4_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 1024);
+  srand(7);
+  for (int n : {64, 128, 256}) {
+    std::vector<int> av(128 * 64), bv(n * 64);
+    std::vector<uint8_t> ap(128 * 32, 0), bp(n * 32, 0);
+    for (int i = 0; i < 128 * 64; ++i) {
+      av[i] = (i % 64 == 63) ? 6 : (rand() % 3) - 1;  // one large element per row
+      ap[i / 2] |= enc(av[i]) << (4 * (i % 2));
+    }
+    for (int i = 0; i < n * 64; ++i) {
+      bv[i] = (i % 64 == 63) ? 6 : (rand() % 3) - 1;
+      bp[i / 2] |= enc(bv[i]) << (4 * (i % 2));
+    }
+    uint8_t *da, *db;
+    float *dout;
+    unsigned long long *dclk;
+    cudaMalloc(&da, ap.size());
+    cudaMalloc(&db, bp.size());
+    cudaMalloc(&dout, 128 * n * 4);
+    cudaMalloc(&dclk, 148 * 8);
+    cudaMemcpy(da, ap.data(), ap.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(db, bp.data(), bp.size(), cudaMemcpyHostToDevice);
+    const int reps = 300;  // |sum| up to 300 * (63 + 36) < 2^24
+    for (int sfc : {1, 2, 4}) for (uint32_t sv : {0u, 0x87878787u}) {
+      fp4_mma<<<1, 128, 32 * 1024>>>(da, db, n, 1, 0, dout, dclk, sfc, sv);
+      std::vector<float> o1(128 * n);
+      cudaMemcpy(o1.data(), dout, o1.size() * 4, cudaMemcpyDeviceToHost);
+      long bad1 = 0;
+      const double mul = sv ? 256.0 : 1.0;
+      for (int r = 0; r < 128; ++r)
+        for (int c = 0; c < n; ++c) {
+          long s1 = 0;
+          for (int k = 0; k < 64; ++k) s1 += long(av[r * 64 + k]) * bv[c * 64 + k];
+          if (double(o1[r * n + c]) != mul * double(s1)) ++bad1;
+        }
+      printf("{\"probe\": \"sf_columns\", \"n\": %d, \"sf_cols_filled\": %d, \"a_scale\": %g, \"mismatches\": %ld}\n", n, sfc, mul, bad1);
+    }
+    fp4_mma<<<1, 128, 32 * 1024>>>(da, db, n, reps, 0, dout, dclk, 32, 0u);
+    std::vector<float> out(128 * n);
+    cudaError_t e = cudaMemcpy(out.data(), dout, out.size() * 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) { printf("{\"error\": \"%s\"}\n", cudaGetErrorString(e)); return 1; }
+    long bad = 0, maxabs = 0;
+    for (int r = 0; r < 128; ++r)
+      for (int c = 0; c < n; ++c) {
+        long s = 0;
+        for (int k = 0; k < 64; ++k) s += long(av[r * 64 + k]) * bv[c * 64 + k];
+        s *= reps;
+        maxabs = std::max(maxabs, std::labs(s));
+        if (double(out[r * n + c]) != double(s)) ++bad;
+      }
+    fp4_mma<<<sms, 128, 32 * 1024>>>(da, db, n, 4096, 1, dout, dclk, 32, 0u);
+    unsigned long long clk[148];
+    cudaMemcpy(clk, dclk, sms * 8, cudaMemcpyDeviceToHost);
+    const double cpm = double(clk[0]) / 4096;
+    printf("{\"bench\": \"mxf4_ss\", \"n\": %d, \"exact_mismatches\": %ld, \"max_abs\": %ld, \"clk_per_mma\": %.1f, "
+           "\"mac_per_clk\": %.0f}\n", n, bad, maxabs, cpm, 128.0 * n * 64 / cpm);
+  }
+  return 0;
+}
