@@ -74,6 +74,7 @@ constexpr int PROD_THREADS = NUM_PROD_WARPS * 32;
 constexpr int EPI_THREADS = NUM_EPI_WARPS * 32;
 constexpr int ACC_COLS = 256;   // one accumulator buffer
 constexpr int FP4_COLS = 248;   // FP4: the last 8 TMEM columns hold the block scales
+                                // (one-buffer mode: 2 * 248 + 8 = 504 accumulator columns)
 constexpr int TMEM_COLS = 512;  // two buffers
 constexpr int MAX_STAGES = 8;
 constexpr int MAX_CHUNKS = 64;  // 32-lane chunks per pixel (2048 lanes)
@@ -118,6 +119,7 @@ struct Params {
   // FP4: raw activation blocks arrive by TMA (one box of 16 B x P x strip rows per stage)
   uint32_t off_rraw, rraw_bytes, rraw_box_bytes;
   int rraw_stages, raw_rows;
+  int nbuf;                 // accumulator buffers: 2 (epilogue overlaps the next tile) or 1 (long K, big M)
   int n_slabs;
   const int8_t *bias_slab;  // [n_slabs][khalf][n_tile][16]: s8, sum(lo) + 127*sum(hi) = bias
   const int32_t *slab_of_nt;
@@ -775,12 +777,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (p.b_resident) mbar_wait(smem_u32(bres), 0);
       int s = 0, ph = 0, it = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-        const int ab = it & 1;
+        const int ab = p.nbuf == 2 ? (it & 1) : 0;
         const int nt = t - fdiv(t, p.nt_magic) * p.n_tiles;
 #ifdef MBU_TIMELINE
         unsigned long long tl0 = clock64();
 #endif
-        mbar_wait(smem_u32(&acc_empty[ab]), (it >> 1) & 1);
+        mbar_wait(smem_u32(&acc_empty[ab]), (p.nbuf == 2 ? (it >> 1) : it) & 1);
 #ifdef MBU_TIMELINE
         unsigned long long tl1 = clock64();
 #endif
@@ -927,15 +929,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_arrive(smem_u32(&acc_empty[ab]));
     };
     init_buffer(blockIdx.x, 0);
-    init_buffer(blockIdx.x + gridDim.x, 1);
+    if (p.nbuf == 2) init_buffer(blockIdx.x + gridDim.x, 1);
     int it = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-      const int ab = it & 1;
+      const int ab = p.nbuf == 2 ? (it & 1) : 0;
       const Tile tl = decode_tile(p, t);
 #ifdef MBU_TIMELINE
       unsigned long long te0 = clock64();
 #endif
-      mbar_wait(smem_u32(&acc_full[ab]), (it >> 1) & 1);
+      mbar_wait(smem_u32(&acc_full[ab]), (p.nbuf == 2 ? (it >> 1) : it) & 1);
 #ifdef MBU_TIMELINE
       unsigned long long te1 = clock64();
 #endif
@@ -1034,7 +1036,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       // buffer drained: re-arm it with the bias of the tile that reuses it
-      init_buffer(t + 2 * gridDim.x, ab);
+      init_buffer(t + p.nbuf * gridDim.x, ab);
 #ifdef MBU_TIMELINE
       if (blockIdx.x == 0 && lane == 0 && it < 64 && warp == 0) {
         g_timeline[it * 12 + 4] = te0;
@@ -1420,7 +1422,12 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   // 3x3 layers run kind::mxf4 (e2m1) when the uniform block-scale columns fit
   // next to the accumulators (MB * n_tile <= 248); MBU_OPT_CONV_I8 forces kind::i8
   const bool fp4 = cv->fp4_ok && !g_force_conv_i8 && tc::FP4_COLS / cv->n_tile >= 1;
-  p.MB = fp4 ? std::min(8, tc::FP4_COLS / cv->n_tile)
+  // long-K FP4 layers (>= 4 K stages) trade the second accumulator for a
+  // taller tile (one buffer of up to 504 columns): each weight stage then
+  // feeds up to 3 (N = 128) or 7 (N = 64) pixel blocks, cutting the weight
+  // stream from L2; the un-overlapped epilogue costs a fraction of such a tile
+  p.nbuf = (fp4 && cv->kp >= 4 && cv->n_tile == 128) ? 1 : 2;
+  p.MB = fp4 ? std::min(8, (p.nbuf == 1 ? 2 * tc::FP4_COLS + 8 : tc::FP4_COLS) / cv->n_tile)
              : std::min(cv->taps == 9 ? 8 : 4, tc::ACC_COLS / cv->n_tile);  // one tap: Q <= 512
   if (x.w >= 128) {
     p.row_mode = 1;
