@@ -49,6 +49,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -59,6 +60,7 @@ namespace mbu {
 namespace tc {
 #ifdef MBU_TIMELINE
 __device__ unsigned long long g_timeline[64 * 12];
+__device__ unsigned long long g_epi[64 * 16];
 #endif
 
 constexpr int BLOCK_M = 128;
@@ -972,7 +974,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (rr < rn.y) {
                 if (rr + 1 < rn.y) {
                   uint32_t v[64];
+#ifdef MBU_TIMELINE
+                  if (blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64 && b < 4 && rr < 4)
+                    g_epi[it * 16 + b * 4 + (rr >> 1) * 2] = clock64();
+#endif
                   tmem_ld64(col0 + uint32_t(rr * 32), v);
+#ifdef MBU_TIMELINE
+                  if (blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64 && b < 4 && rr < 4)
+                    g_epi[it * 16 + b * 4 + (rr >> 1) * 2 + 1] = clock64();
+#endif
                   w8[rr] = pack_nonneg<0>(v);
                   w8[rr + 1] = pack_nonneg<32>(v);
                 } else {
@@ -1392,7 +1402,17 @@ static int launch_tc_impl(const tc::Params &p, const CUtensorMap &xmap, int grid
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(h, tc::g_timeline, sizeof(h));
     const unsigned long long b0 = h[0];
-    fprintf(stderr, "TIMELINE call %d taps %d fp4 %d MB %d ntile %d ks %d\n", call++, TAPS, int(FP4), p.MB, p.n_tile, p.ks);
+    fprintf(stderr, "TIMELINE call %d taps %d fp4 %d MB %d ntile %d ks %d\n", call, TAPS, int(FP4), p.MB, p.n_tile, p.ks);
+    {
+      unsigned long long e[64 * 16];
+      cudaMemcpyFromSymbol(e, tc::g_epi, sizeof(e));
+      for (int i = 2; i < 5; ++i) {
+        fprintf(stderr, "  epi it %d:", i);
+        for (int k = 0; k < 16; ++k) fprintf(stderr, " %lld", (long long)(e[i * 16 + k] ? e[i * 16 + k] - h[0] : 0));
+        fprintf(stderr, "\n");
+      }
+    }
+    ++call;
     for (int i = 0; i < 24; ++i)
       fprintf(stderr, "  it %2d mma: waitE %6lld got %6lld fullL %6lld issued %6lld | epi0: wait %6lld got %6lld done %6lld | epi4 done %6lld | prod stage %2d: start %6lld emptyok %6lld end %6lld\n", i,
               (long long)(h[i * 12] - b0), (long long)(h[i * 12 + 1] - b0), (long long)(h[i * 12 + 3] - b0),

@@ -1,4 +1,8 @@
-"""Per-tile MMA / epilogue timestamps of CTA 0 (needs a -DMBU_TIMELINE build via MBU_LIB)."""
+"""Per-tile MMA / epilogue / producer timestamps of CTA 0 for every conv_tc launch of one
+forward (stderr). Needs a library built with -DMBU_TIMELINE, e.g.
+  nvcc ... -DMBU_TIMELINE -c csrc/conv_tc.cu; link with the other objects into build/ab/tl.so
+  MBU_LIB=build/ab/tl.so python tools/timeline_probe.py 2> timeline.txt
+"""
 import sys
 from pathlib import Path
 
