@@ -330,25 +330,35 @@ def run_ours(args):
         dm.set_timing(False)
         lt = [x / reps for x in acc_t]
         ops = layer_ops(model, BATCH)
-        tc_ops = sum(o for o, l in zip(ops, model.layers) if "conv" in l.kind and l.kind != "float-conv")
-        tc_ms = sum(t for t, l in zip(lt, model.layers) if "conv" in l.kind and l.kind != "float-conv")
+        # dominant kernel: the 3x3 binary convs (conv_tc_kernel<9>, tcgen05 kind::mxf4 with
+        # e2m1 operands, 17 launches per step); the 2x2/s2 tconvs run kind::i8 (4 launches)
+        fp4 = not os.environ.get("MBU_CONV_I8")
+        is3 = [("conv" in l.kind and l.kind != "float-conv" and "tconv" not in l.kind) for l in model.layers]
+        c3_ops = sum(o for o, k in zip(ops, is3) if k)
+        c3_ms = sum(t for t, k in zip(lt, is3) if k)
         step_ms = sum(lt)
         peaks, src = _peaks()
-        peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-        achieved = tc_ops / (tc_ms / 1e3) / 1e12
+        bf16 = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+        peak = (4.0 if fp4 else 2.0) * bf16
+        achieved = c3_ops / (c3_ms / 1e3) / 1e12
         breakdown = [
             {"layer": l.name, "kind": l.kind, "ms": round(t, 4),
              "tops": round(o / (t / 1e3) / 1e12, 1) if o and t > 0 else None}
             for l, t, o in zip(model.layers, lt, ops) if l.kind != "concat"]
         roofline = {
-            "bound": "tensor", "kernel": "conv_tc_kernel (tcgen05.mma kind::i8, UTCIMMA)",
+            "bound": "tensor",
+            "kernel": ("conv_tc_kernel<9> 3x3 binary convs (tcgen05.mma kind::mxf4, e2m1 "
+                       "{-1,0,+1} x {0,1}, exact f32 integer accumulation)" if fp4 else
+                       "conv_tc_kernel<9> 3x3 binary convs (tcgen05.mma kind::i8)"),
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": _profile_traffic(),
-            "peak_source": f"2 x bf16_tflops_sustained of {src} MEASURED_PEAKS.json "
-                           "(sm_100 dense int8 rate = 2x bf16)",
-            "ops_per_launch_basis": "2*MAC with the reference's real K (planner.total_ops) "
-                                    "summed over the 21 bit conv/tconv launches of one step",
-            "share_of_step": tc_ms / step_ms,
+            "peak_source": (f"{'4' if fp4 else '2'} x bf16_tflops_sustained of {src} MEASURED_PEAKS.json "
+                            f"(sm_100 dense {'FP4' if fp4 else 'int8'} rate = {'4' if fp4 else '2'}x bf16; "
+                            "tools/ubench_fp4 measures 16368 e2m1 MAC/clk/SM = the nominal FP4 rate)"),
+            "ops_per_launch_basis": "2*MAC with the reference's real K (planner.total_ops) summed over "
+                                    "the 17 3x3 conv launches of one step, over their summed CUDA-event time",
+            "share_of_step": c3_ms / step_ms,
+            "launches": int(sum(is3)),
         }
         cudnn = None
         if not args.no_cudnn and world == 1:
@@ -377,7 +387,9 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "s8 (tcgen05 kind::i8, s32 acc) / u64 bitplanes / f64 endpoints",
+            "vs_baseline": None,
+            "dtype": "e2m1 (tcgen05 kind::mxf4, exact f32 integer acc) 3x3 convs / s8 (kind::i8, s32 acc) "
+                     "tconvs / u64 bitplanes / f64 endpoints",
             "data": "synthetic: live-generator random weights (seed 0), uniform [0,1) float64 images",
             "config": {"workload": "MBU-Net forward, batch 8 per GPU, 3x1024x2048 (config 3; "
                                    "config 4 when N>1)", "global_batch": BATCH * world,

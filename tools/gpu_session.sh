@@ -15,6 +15,8 @@ fi
 if [ "${SKIP_NCU:-0}" != 1 ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $OUT/launches.csv python tools/profile_forward.py --reps 1 > $OUT/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
+timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+  -k regex:conv_tc --csv --log-file $OUT/conv_traffic.csv python tools/profile_forward.py --reps 1 > $OUT/ncu_traffic.log 2>&1; echo "ncu traffic rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:conv_tc -s ${NCU_SKIP:-2} -c ${NCU_COUNT:-3} \
   -o $OUT/prof_conv_tc -f python tools/profile_forward.py --reps 1 > $OUT/ncu_full.log 2>&1; echo "ncu full rc=$?"
 fi
