@@ -85,6 +85,7 @@ from .quantizer import (
     quantize_bundle,
     synthesize_bundle,
 )
+from .modelfile import read_model, read_tensor, write_model, write_tensor
 from .runtime import DeviceModel, Engine
 
 __all__ = [
@@ -103,5 +104,6 @@ __all__ = [
     "transposed_conv_forward", "xor_popcount_rows",
     "BundleEntry", "WeightBundle", "dense_records", "live_bundle", "quantize_bundle",
     "synthesize_bundle",
+    "read_model", "read_tensor", "write_model", "write_tensor",
     "DeviceModel", "Engine",
 ]

@@ -178,3 +178,17 @@ def test_fast_endpoints_equal_float64_endpoints_full_width(cuda):
         _lib.call("mbu_set_option", 1, 0)
     assert np.array_equal(a.mask, b.mask)
     assert np.allclose(a.logits, b.logits, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["tiny_masked", "tiny_binary_f2", "tiny_masked_zero"])
+def test_forward_of_reference_model_file(cuda, name):
+    """A model file written by the reference (bitunet.modelfile.write_model)
+    runs on the GPU unchanged: mask exact, logits within 1e-9 of the
+    reference's own forward."""
+    from conftest import GOLDEN
+
+    z = np.load(GOLDEN / "modelfile_forward.npz")
+    model = mb.read_model(GOLDEN / f"{name}.mbun")
+    res = mb.forward(model, z["image"], device="cuda:0")
+    assert np.array_equal(res.mask, z[f"{name}/mask"])
+    assert np.allclose(res.logits, z[f"{name}/logits"], rtol=1e-9, atol=1e-9)
