@@ -140,6 +140,13 @@ int mbu_fconv_run(mbu_fconv *conv, const double *x_f64, const uint64_t *x_bits,
                   double *acc_out, uint64_t *bits_out, int out_stride,
                   int out_offset, uint8_t *mask_out, void *stream);
 
+/* Class map of a multi-class head (an extra, not a
+ * reference entry point: the reference's mask is per channel, graph.py:455).
+ * classes[p] = first index of the largest logits[p, :] (NaN counts as the
+ * largest, like numpy.argmax). channels <= 256. */
+int mbu_argmax(const double *logits, int64_t pixels, int channels, uint8_t *classes,
+               void *stream);
+
 /* ------------------------------------------------------------------ */
 /* Whole-network runner (graph.py:413-458 forward)                     */
 /* ------------------------------------------------------------------ */

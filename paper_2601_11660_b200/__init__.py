@@ -69,6 +69,7 @@ from .layers import (
 )
 from .ops import (
     apply_threshold,
+    argmax_classes,
     bit_gemm,
     conv_forward,
     float_bn_sign,
@@ -100,7 +101,7 @@ __all__ = [
     "CONST_NEG", "CONST_POS", "DIR_GE", "DIR_LE", "ConvSpec", "FusedThreshold",
     "concat_channels", "fuse_bn_sign", "pack_conv_weights", "unpack_conv_weights",
     "weight_position_sums",
-    "apply_threshold", "bit_gemm", "conv_forward", "float_bn_sign", "float_conv", "maxpool2",
+    "apply_threshold", "argmax_classes", "bit_gemm", "conv_forward", "float_bn_sign", "float_conv", "maxpool2",
     "transposed_conv_forward", "xor_popcount_rows",
     "BundleEntry", "WeightBundle", "dense_records", "live_bundle", "quantize_bundle",
     "synthesize_bundle",

@@ -335,3 +335,36 @@ int launch_head_fast(const mbu_fconv *fc, const ActView &xb, int n, int h, int w
 }
 
 }  // namespace mbu
+
+// ---------------------------------------------------------------------------
+// class map of a multi-class head: numpy.argmax over the channel axis
+// ---------------------------------------------------------------------------
+namespace mbu {
+__global__ void __launch_bounds__(256) argmax_kernel(const double *__restrict__ logits, int64_t pixels,
+                                                     int c, uint8_t *__restrict__ classes) {
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < pixels;
+       p += int64_t(gridDim.x) * blockDim.x) {
+    const double *row = logits + p * c;
+    double best = row[0];
+    int idx = 0;
+    for (int k = 1; k < c && best == best; ++k) {  // a NaN wins and stops the scan
+      const double v = __ldg(row + k);
+      if (v != v || v > best) {
+        best = v;
+        idx = k;
+      }
+    }
+    classes[p] = uint8_t(idx);
+  }
+}
+}  // namespace mbu
+
+extern "C" int mbu_argmax(const double *logits, int64_t pixels, int channels, uint8_t *classes,
+                          void *stream) {
+  using namespace mbu;
+  if (channels < 1 || channels > 256) return fail(MBU_ERR_SHAPE, "argmax: channels must be 1..256");
+  if (pixels <= 0) return MBU_OK;
+  const int64_t blocks = std::min<int64_t>((pixels + 255) / 256, 148 * 16);
+  argmax_kernel<<<unsigned(blocks), 256, 0, as_stream(stream)>>>(logits, pixels, channels, classes);
+  return check_launch("argmax_kernel");
+}

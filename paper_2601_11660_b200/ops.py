@@ -337,3 +337,22 @@ def bit_gemm(a: PackedBitMatrix, b_pos: PackedBitMatrix, b_neg, k_true: int, thr
                 - xor_popcount_rows(a.words, b_pos.words, device=device))
     d = xor_popcount_rows(a.words, b_pos.words, device=device)
     return (np.int32(k_true) - 2 * d).astype(np.int32)
+
+
+def argmax_classes(logits, *, device=None):
+    """Class map of a multi-class head (an extra on
+    top of the reference's per-channel ``logits >= 0`` mask): uint8
+    (n, H, W) = ``numpy.argmax(logits, axis=-1)``, computed by
+    ``mbu_argmax``. A CUDA tensor stays on its device; anything else is
+    uploaded and the result returned as a NumPy array."""
+    on_dev = isinstance(logits, torch.Tensor) and logits.is_cuda
+    dev = logits.device if on_dev else cuda_device(device)
+    t = logits if on_dev else torch.from_numpy(np.ascontiguousarray(logits, dtype=np.float64)).to(dev)
+    if t.dtype != torch.float64 or t.ndim < 1:
+        raise ShapeError(f"logits must be float64 with a channel axis, got {t.dtype} {tuple(t.shape)}")
+    t = t.contiguous()
+    c = t.shape[-1]
+    out = torch.empty(t.shape[:-1], dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        _lib.call("mbu_argmax", _ptr(t), out.numel(), c, _ptr(out), _stream(dev))
+    return out if on_dev else out.cpu().numpy()

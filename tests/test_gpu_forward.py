@@ -192,3 +192,29 @@ def test_forward_of_reference_model_file(cuda, name):
     res = mb.forward(model, z["image"], device="cuda:0")
     assert np.array_equal(res.mask, z[f"{name}/mask"])
     assert np.allclose(res.logits, z[f"{name}/logits"], rtol=1e-9, atol=1e-9)
+
+
+@pytest.mark.parametrize("classes", [3, 19])
+def test_multiclass_head_and_class_map(cuda, classes):
+    """Multi-class head: per-channel logits / masks
+    against the dense oracle, and the argmax class map against numpy
+    (including a NaN logit, which numpy.argmax picks first)."""
+    from dataclasses import replace
+
+    cfg = replace(tiny_config(extent=32), out_channels=classes)
+    rng = np.random.default_rng(40 + classes)
+    bundle = mb.live_bundle(cfg, rng)
+    model = mb.build(cfg, bundle)
+    image = rng.random((2, 32, 32, 3))
+    res = mb.forward(model, image, device="cuda:0")
+    ref = dense.ref_forward(cfg, mb.dense_records(mb.quantize_bundle(bundle, cfg), cfg), image)
+    assert res.logits.shape == (2, 32, 32, classes)
+    assert np.array_equal(res.mask, ref["mask"])
+    assert np.allclose(res.logits, ref["head"]["out"], rtol=1e-9, atol=1e-9)
+    lg = res.logits.copy()
+    lg[0, 1, 2, classes // 2] = np.nan
+    lg[1, 3, 4, :] = 0.25  # ties: first index
+    got = mb.argmax_classes(lg, device="cuda:0")
+    assert got.dtype == np.uint8 and np.array_equal(got, np.argmax(lg, axis=-1))
+    gd = mb.argmax_classes(torch.from_numpy(lg).to(cuda))
+    assert gd.is_cuda and np.array_equal(gd.cpu().numpy(), np.argmax(lg, axis=-1))
