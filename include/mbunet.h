@@ -147,6 +147,12 @@ int mbu_fconv_run(mbu_fconv *conv, const double *x_f64, const uint64_t *x_bits,
 int mbu_argmax(const double *logits, int64_t pixels, int channels, uint8_t *classes,
                void *stream);
 
+/* Netpbm raster -> float64 image (imageio.py:59-83 read_image): out[i] =
+ * sample[i] / maxval, samples u8 (bytes_per_sample 1) or big-endian u16 (2),
+ * the same correctly rounded float64 division as the reference. */
+int mbu_decode_raster(const void *raster, int64_t count, int bytes_per_sample, int maxval,
+                      double *out, void *stream);
+
 /* ------------------------------------------------------------------ */
 /* Whole-network runner (graph.py:413-458 forward)                     */
 /* ------------------------------------------------------------------ */

@@ -67,9 +67,11 @@ from .layers import (
     unpack_conv_weights,
     weight_position_sums,
 )
+from .imageio import read_image, read_raster, write_gray, write_mask
 from .ops import (
     apply_threshold,
     argmax_classes,
+    decode_raster,
     bit_gemm,
     conv_forward,
     float_bn_sign,
@@ -101,6 +103,7 @@ __all__ = [
     "CONST_NEG", "CONST_POS", "DIR_GE", "DIR_LE", "ConvSpec", "FusedThreshold",
     "concat_channels", "fuse_bn_sign", "pack_conv_weights", "unpack_conv_weights",
     "weight_position_sums",
+    "read_image", "read_raster", "write_gray", "write_mask", "decode_raster",
     "apply_threshold", "argmax_classes", "bit_gemm", "conv_forward", "float_bn_sign", "float_conv", "maxpool2",
     "transposed_conv_forward", "xor_popcount_rows",
     "BundleEntry", "WeightBundle", "dense_records", "live_bundle", "quantize_bundle",

@@ -368,3 +368,58 @@ extern "C" int mbu_argmax(const double *logits, int64_t pixels, int channels, ui
   argmax_kernel<<<unsigned(blocks), 256, 0, as_stream(stream)>>>(logits, pixels, channels, classes);
   return check_launch("argmax_kernel");
 }
+
+// ---------------------------------------------------------------------------
+// netpbm raster -> float64 image (imageio.py:59-83): sample / maxval
+// ---------------------------------------------------------------------------
+namespace mbu {
+__global__ void __launch_bounds__(256) decode_u8_kernel(const uchar4 *__restrict__ in, int64_t quads,
+                                                        double maxval, double4 *__restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < quads;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uchar4 v = in[i];
+    out[i] = make_double4(__ddiv_rn(double(v.x), maxval), __ddiv_rn(double(v.y), maxval),
+                          __ddiv_rn(double(v.z), maxval), __ddiv_rn(double(v.w), maxval));
+  }
+}
+__global__ void __launch_bounds__(256) decode_tail_kernel(const uint8_t *__restrict__ in, int64_t begin,
+                                                          int64_t count, int bps, double maxval,
+                                                          double *__restrict__ out) {
+  for (int64_t i = begin + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t v = bps == 1 ? in[i] : (uint32_t(in[2 * i]) << 8) | in[2 * i + 1];  // big endian
+    out[i] = __ddiv_rn(double(v), maxval);
+  }
+}
+}  // namespace mbu
+
+extern "C" int mbu_decode_raster(const void *raster, int64_t count, int bytes_per_sample, int maxval,
+                                 double *out, void *stream) {
+  using namespace mbu;
+  if (bytes_per_sample != 1 && bytes_per_sample != 2)
+    return fail(MBU_ERR_SHAPE, "decode_raster: 1 or 2 bytes per sample");
+  if (maxval < 1 || maxval > 65535 || (bytes_per_sample == 1 && maxval > 255))
+    return fail(MBU_ERR_SHAPE, "decode_raster: maxval out of range");
+  if (count <= 0) return MBU_OK;
+  cudaStream_t st = as_stream(stream);
+  const auto *in = static_cast<const uint8_t *>(raster);
+  int64_t done = 0;
+  if (bytes_per_sample == 1 && (reinterpret_cast<uintptr_t>(in) & 3) == 0 &&
+      (reinterpret_cast<uintptr_t>(out) & 31) == 0) {
+    const int64_t quads = count / 4;
+    if (quads) {
+      const int64_t blocks = std::min<int64_t>((quads + 255) / 256, 148 * 32);
+      decode_u8_kernel<<<unsigned(blocks), 256, 0, st>>>(reinterpret_cast<const uchar4 *>(in), quads,
+                                                        double(maxval), reinterpret_cast<double4 *>(out));
+      MBU_TRY(check_launch("decode_u8_kernel"));
+    }
+    done = quads * 4;
+  }
+  if (done < count) {
+    const int64_t blocks = std::min<int64_t>((count - done + 255) / 256, 148 * 32);
+    decode_tail_kernel<<<unsigned(blocks), 256, 0, st>>>(in, done, count, bytes_per_sample, double(maxval),
+                                                         out);
+    MBU_TRY(check_launch("decode_tail_kernel"));
+  }
+  return MBU_OK;
+}

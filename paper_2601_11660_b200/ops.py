@@ -356,3 +356,29 @@ def argmax_classes(logits, *, device=None):
     with torch.cuda.device(dev):
         _lib.call("mbu_argmax", _ptr(t), out.numel(), c, _ptr(out), _stream(dev))
     return out if on_dev else out.cpu().numpy()
+
+
+def decode_raster(raster, maxval: int, *, out=None, device=None):
+    """Netpbm samples -> float64 image on the GPU (``mbu_decode_raster``):
+    ``sample / maxval``, bit-identical to ``read_image`` / the reference's
+    ``imageio.read_image`` (imageio.py:59-83). ``raster`` is what
+    ``imageio.read_raster`` returns (u8 (n, h, w, c), or (n, h, w, c, 2)
+    big-endian byte pairs) as a NumPy array or a CUDA uint8 tensor; ``out``
+    an optional float64 CUDA tensor of shape (n, h, w, c)."""
+    on_dev = isinstance(raster, torch.Tensor) and raster.is_cuda
+    dev = raster.device if on_dev else cuda_device(device)
+    r = raster if on_dev else torch.from_numpy(np.ascontiguousarray(raster, dtype=np.uint8)).to(dev)
+    if r.dtype != torch.uint8:
+        raise ShapeError(f"raster must be uint8, got {r.dtype}")
+    r = r.contiguous()
+    bps = 2 if maxval > 255 else 1
+    shape = tuple(r.shape[:-1]) if bps == 2 else tuple(r.shape)
+    if bps == 2 and r.shape[-1] != 2:
+        raise ShapeError("16-bit rasters carry a trailing axis of 2 bytes")
+    if out is None:
+        out = torch.empty(shape, dtype=torch.float64, device=dev)
+    elif tuple(out.shape) != shape or out.dtype != torch.float64 or not out.is_contiguous():
+        raise ShapeError(f"out must be a contiguous float64 tensor of shape {shape}")
+    with torch.cuda.device(dev):
+        _lib.call("mbu_decode_raster", _ptr(r), out.numel(), bps, int(maxval), _ptr(out), _stream(dev))
+    return out

@@ -322,6 +322,53 @@ class Engine:
                 ev["d2h"][s].record(self.d2h)
             self._used[s] = True
 
+    def run_stream_raster(self, host_rasters, maxval: int, host_logits, host_masks, steps: int):
+        """``run_stream`` for frame streams in netpbm sample form (SURVEY.md
+        §8(f) rank 2): step i uploads the pinned uint8 raster
+        ``host_rasters[i % len]`` of shape (batch, H, W, C) (or (batch, H, W, C, 2) for
+        16-bit samples; 1-2 bytes per sample instead of 8), decodes it on the GPU into the image buffer
+        (``decode_raster``: sample / maxval, the reference's read_image
+        arithmetic), then runs the forward and downloads as ``run_stream``."""
+        from .ops import decode_raster
+
+        self._ensure_slots()
+        rshape = tuple(host_rasters[0].shape)
+        if rshape not in (self.shape, self.shape + (2,)):
+            raise ShapeError(f"raster batches must be {self.shape} (+ (2,) for 16-bit), got {rshape}")
+        if getattr(self, "_raster_slots", None) is None or tuple(self._raster_slots[0].shape) != rshape:
+            self._raster_slots = [torch.empty(rshape, dtype=torch.uint8, device=self.device)
+                                  for _ in range(2)]
+        ev = self._ev
+        for i in range(steps):
+            s = i & 1
+            img, lg, mk, g = self._slots[s]
+            rs = self._raster_slots[s]
+            hr = host_rasters[i % len(host_rasters)]
+            hl = None if host_logits is None else host_logits[i % len(host_logits)]
+            hm = host_masks[i % len(host_masks)]
+            with torch.cuda.stream(self.h2d):
+                if self._used[s]:
+                    self.h2d.wait_event(ev["comp"][s])
+                rs.copy_(hr, non_blocking=True)
+                ev["h2d"][s].record(self.h2d)
+            with torch.cuda.stream(self.stream):
+                self.stream.wait_event(ev["h2d"][s])
+                if self._used[s]:
+                    self.stream.wait_event(ev["d2h"][s])
+                decode_raster(rs, maxval, out=img)
+                if g is not None:
+                    g.replay()
+                else:
+                    self._enqueue(img, lg, mk)
+                ev["comp"][s].record(self.stream)
+            with torch.cuda.stream(self.d2h):
+                self.d2h.wait_event(ev["comp"][s])
+                if hl is not None:
+                    hl.copy_(lg, non_blocking=True)
+                hm.copy_(mk, non_blocking=True)
+                ev["d2h"][s].record(self.d2h)
+            self._used[s] = True
+
     def run(self):
         with torch.cuda.stream(self.stream):
             if self.graph is not None:
