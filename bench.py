@@ -313,6 +313,27 @@ def run_ours(args):
                       "forward, float64 logits + uint8 mask D2H on a second copy stream; two "
                       "device buffer sets overlap step i's compute with i+1's upload / i-1's "
                       "download"}
+        # same loop fed with 8-bit netpbm samples, decoded on the GPU (decode_raster)
+        host_r = [torch.empty(eng.shape, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        for hr in host_r:
+            hr.copy_(torch.randint(0, 256, eng.shape, dtype=torch.uint8, device=dev, generator=g).cpu())
+        eng.run_stream_raster(host_r, 255, host_logits, host_masks, args.warmup)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(eng.h2d)
+        eng.run_stream_raster(host_r, 255, host_logits, host_masks, args.steps)
+        e1.record(eng.d2h)
+        torch.cuda.synchronize()
+        barrier()
+        r_ms = max_over_ranks(e0.elapsed_time(e1))
+        e2e["raster_u8"] = {
+            "value": world * BATCH * args.steps / (r_ms / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": host_r[0].numel(),
+            "d2h_bytes_per_step": host_logits[0].numel() * 8 + host_masks[0].numel(),
+            "ms_per_step": r_ms / args.steps,
+            "how": "Engine.run_stream_raster: pinned 8-bit P6 samples H2D, mbu_decode_raster "
+                   "(sample/255, bit-identical to read_image) + forward, same D2H"}
     clk = clocks.stop()
 
     line = None
