@@ -187,19 +187,33 @@ def _device_model(model, device) -> DeviceModel:
 
 def forward(model, image, threads: int = 1, trace: bool = False, *, device=None,
             path=_lib.PATH_AUTO):
-    """Run the compiled network on an (n, H, W, C) float64 image, on the GPU."""
+    """Run the compiled network on an (n, H, W, C) float64 image, on the GPU.
+
+    ``image`` is a host array (uploaded here) or a float64 CUDA tensor already
+    on the device (e.g. from ``decode_raster``), used in place."""
     cfg = model.config
-    image = np.asarray(image, dtype=np.float64)
-    if image.ndim != 4 or image.shape[1:] != (cfg.height, cfg.width, cfg.in_channels):
+    on_dev = isinstance(image, torch.Tensor) and image.is_cuda
+    if on_dev:
+        if image.dtype != torch.float64:
+            raise ShapeError(f"device image must be float64, got {image.dtype}")
+        device = image.device if device is None else device
+    else:
+        image = np.asarray(image, dtype=np.float64)
+    if image.ndim != 4 or tuple(image.shape[1:]) != (cfg.height, cfg.width, cfg.in_channels):
         raise ShapeError(
-            f"image shape {image.shape} != (n, {cfg.height}, {cfg.width}, {cfg.in_channels})")
+            f"image shape {tuple(image.shape)} != (n, {cfg.height}, {cfg.width}, {cfg.in_channels})")
     dm = _device_model(model, device)
     n = image.shape[0]
     dev = dm.device
     ws_bytes = dm.plan(n, cfg.height, cfg.width, trace)
     with torch.cuda.device(dev):
         ws = torch.empty(max(ws_bytes, 8) // 8 + 1, dtype=torch.int64, device=dev)
-        img = torch.from_numpy(np.ascontiguousarray(image)).to(dev)
+        if on_dev:
+            if image.device != dev:
+                raise ShapeError(f"image is on {image.device}, model runs on {dev}")
+            img = image.contiguous()
+        else:
+            img = torch.from_numpy(np.ascontiguousarray(image)).to(dev)
         out_c = cfg.out_channels
         logits = torch.empty((n, cfg.height, cfg.width, out_c), dtype=torch.float64, device=dev)
         mask = torch.empty((n, cfg.height, cfg.width, out_c), dtype=torch.uint8, device=dev)

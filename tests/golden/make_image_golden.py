@@ -6,7 +6,9 @@
 Writes ``img_rgb8.ppm`` (P6, maxval 255, header comments), ``img_gray16.pgm``
 (P5, maxval 1000, big-endian 16-bit samples), ``img_rgb7.ppm`` (maxval 7) and
 ``images.npz`` with the reference's ``read_image`` of each, plus the bytes of
-its ``write_mask`` / ``write_gray`` on fixed inputs.
+its ``write_mask`` / ``write_gray`` on fixed inputs; ``cli_mask.pgm`` /
+``cli_logits.rten``: the reference ``bitunet infer`` of ``tiny_masked.mbun``
+on ``img_32.ppm``.
 """
 
 from __future__ import annotations
@@ -43,6 +45,16 @@ def main():
     (OUT / "tmp_mask.pgm").unlink()
     (OUT / "tmp_gray.pgm").unlink()
     np.savez_compressed(OUT / "images.npz", **arrays)
+
+    # the reference CLI end to end on a reference-written model (cli.py:268-288)
+    from bitunet.cli import main as ref_main
+
+    img = rng.integers(0, 256, size=(32, 32, 3), dtype=np.uint8)
+    (OUT / "img_32.ppm").write_bytes(b"P6\n32 32\n255\n" + img.tobytes())
+    rc = ref_main(["infer", "--model", str(OUT / "tiny_masked.mbun"), "--image", str(OUT / "img_32.ppm"),
+                   "--mask-out", str(OUT / "cli_mask.pgm"), "--logits-out", str(OUT / "cli_logits.rten"),
+                   "--threads", "1"])
+    assert rc == 0, rc
 
 
 if __name__ == "__main__":
