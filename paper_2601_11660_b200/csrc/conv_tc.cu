@@ -56,11 +56,32 @@
 
 #include "common.cuh"
 
+// largest FP4 bias-slab set kept resident in shared memory (64 B per GEMM
+// column: 512 output channels); launch falls back to kind::i8 if a geometry
+// then leaves fewer than two pipeline stages
+#ifndef MBU_FP4_SLAB_CAP
+#define MBU_FP4_SLAB_CAP 32768
+#endif
 namespace mbu {
 namespace tc {
 #ifdef MBU_TIMELINE
 __device__ unsigned long long g_timeline[64 * 12];
 __device__ unsigned long long g_epi[64 * 16];
+#define MMA_T(slot)                                                          \
+  do {                                                                       \
+    if (blockIdx.x == 0 && lane == 0 && it < 64 && (slot) < 16) g_epi[it * 16 + (slot)] = clock64(); \
+  } while (0)
+#define EPI_T(slot)                                                                                 \
+  do {                                                                                              \
+    if (blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64) g_epi[it * 16 + (slot)] = clock64(); \
+  } while (0)
+#else
+#define EPI_T(slot) \
+  do {              \
+  } while (0)
+#define MMA_T(slot) \
+  do {              \
+  } while (0)
 #endif
 
 constexpr int BLOCK_M = 128;
@@ -639,6 +660,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int g = 0; g < LA; ++g) issue();
     }
     for (int g = 0; g < n_stages_total; ++g) {
+      // FP4: this stage's chunk pair (read before the waits, off the expansion's path)
+      const int ca = FP4 ? chunk_s[2 * e_k] & 3 : 0, cb = FP4 ? chunk_s[2 * e_k + 1] & 3 : 0;
       if constexpr (!FP4) {
         issue();
         asm volatile("cp.async.wait_group %0;" ::"n"(LA) : "memory");  // group g landed
@@ -660,11 +683,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // were zero-filled by cp.async, which expands to 0 in u8 mode; s8 mode
       // masks them explicitly. Indices are clamped so every load is in range.
       const int qmax = p.Q - 1;
+#ifdef ABL_NO_EXPAND
+      if (false) {
+#else
       if constexpr (FP4) {
+#endif
         // two 32-lane chunks -> one K = 64 e2m1 row: chunk c fills core-matrix column c
         // raw box: 16 B (a 128-lane block) per strip pixel, pixels row-major
         const uint32_t lut = p.u8_act ? 0x22200200u : 0x222AA2AAu;
-        const int ca = chunk_s[2 * e_k] & 3, cb = chunk_s[2 * e_k + 1] & 3;
         const int qbox = p.raw_rows * p.P - 1;
 #pragma unroll
         for (int j = 0; j < PI; ++j) {
@@ -781,6 +807,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         const int ab = p.nbuf == 2 ? (it & 1) : 0;
         const int nt = t - fdiv(t, p.nt_magic) * p.n_tiles;
+        // (read before the wait: a shared load issued behind the tensor core's
+        // operand reads takes hundreds of cycles, keep it off the issue path)
+        const int slab = p.mma_bias ? smap[nt] : 0;
 #ifdef MBU_TIMELINE
         unsigned long long tl0 = clock64();
 #endif
@@ -790,22 +819,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
         tc_fence_after();
         const uint32_t d0 = tmem + uint32_t(ab * ACC_COLS);
-        if constexpr (FP4) {  // bias = lo (scale 1) + 256 * hi (A scale 2^8)
-          const uint64_t sd = slab_desc0 + uint64_t(smap[nt]) * uint64_t(p.n_tile * 4);
+        if (FP4 && p.mma_bias) {  // bias = lo (scale 1) + 256 * hi (A scale 2^8)
+          const uint64_t sd = slab_desc0 + uint64_t(slab) * uint64_t(p.n_tile * 4);
           for (int b = 0; b < p.MB; ++b) {
             umma1_fp4(d0 + uint32_t(b * p.n_tile), ones_desc, sd, p.idesc, tmem + p.sf1, tmem + p.sf1, 0u);
             umma1_fp4(d0 + uint32_t(b * p.n_tile), ones_desc, sd + uint64_t(p.n_tile * 2), p.idesc,
                       tmem + p.sf256, tmem + p.sf1, 1u);
           }
         } else if (p.mma_bias) {
-          const uint64_t sd = slab_desc0 + uint64_t(smap[nt]) * uint64_t(p.n_tile * 2);
+          const uint64_t sd = slab_desc0 + uint64_t(slab) * uint64_t(p.n_tile * 2);
           for (int b = 0; b < p.MB; ++b) umma1_i8_first(d0 + uint32_t(b * p.n_tile), ones_desc, sd, p.idesc);
         }
 #ifdef MBU_TIMELINE
         unsigned long long tl_full = 0;
 #endif
+        MMA_T(0);
         for (int k = 0; k < p.ks; ++k) {
           mbar_wait(smem_u32(&full[s]), ph);
+          if (k == 0) MMA_T(1);
 #ifdef MBU_TIMELINE
           if (k == p.ks - 1) tl_full = clock64();
 #endif
@@ -814,10 +845,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint64_t a_s = a_desc0 + uint64_t((size_t(s) * p.a_stage_bytes) >> 4);
           const uint64_t b_s =
               b_desc0 + uint64_t(((p.b_resident ? size_t(nt * p.ks + k) : size_t(s)) * p.b_stage_bytes) >> 4);
+#ifdef ABL_NO_MMA9
+          if (false) {
+#else
           if constexpr (FP4) {
-            for (int b = 0; b < p.MB; ++b)
+#endif
+            for (int b = 0; b < p.MB; ++b) {
               umma9_fp4(d0 + uint32_t(b * p.n_tile), a_s + uint64_t(block_q0(p, b)), b_s, pp, bs, p.idesc,
                         tmem + p.sf1);
+              if (k == 0) MMA_T(2 + b);
+            }
           } else if (TAPS == 9) {
             for (int b = 0; b < p.MB; ++b)
               umma9_i8(d0 + uint32_t(b * p.n_tile), a_s + uint64_t(block_q0(p, b)), b_s, pp, bs, p.idesc);
@@ -836,6 +873,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         umma_commit_elect(smem_u32(&acc_full[ab]));
+        MMA_T(12);
 #ifdef MBU_TIMELINE
         if (blockIdx.x == 0 && lane == 0 && it < 64) {
           g_timeline[it * 12 + 0] = tl0;
@@ -921,6 +959,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 v[4 * i + 2] = q4.z;
                 v[4 * i + 3] = q4.w;
               }
+              if constexpr (FP4) {  // f32 accumulator: bias + 1/2 (exact, never a signed zero)
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(float(int(v[i])) + 0.5f);
+              }
               tmem_st32(lane_base + uint32_t(ab * ACC_COLS + b * p.n_tile + gg * 32), v);
             }
           }
@@ -936,6 +978,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
       const int ab = p.nbuf == 2 ? (it & 1) : 0;
       const Tile tl = decode_tile(p, t);
+      // a conv tile is one run of its N tile's groups: no shared-memory table
+      // reads on the epilogue path (they queue behind the tensor core's
+      // operand reads); tconv runs are read before the wait
+      const int4 *rt = runs_s + tl.nt * 9 + 1;
+      const int nr = TCONV ? runs_s[tl.nt * 9].x : 1;
 #ifdef MBU_TIMELINE
       unsigned long long te0 = clock64();
 #endif
@@ -943,10 +990,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #ifdef MBU_TIMELINE
       unsigned long long te1 = clock64();
 #endif
+      EPI_T(5);
       tc_fence_after();
+      EPI_T(6);
       const int jt = tl.nt * p.n_tile;
-      const int4 *rt = runs_s + tl.nt * 9 + 1;
-      const int nr = runs_s[tl.nt * 9].x;
       // units (block b, run ri): by block parity when MB >= 2, else by run parity
       const bool split_b = !TCONV || p.MB >= 2;  // (a conv's N tile <= 128: MB >= 2)
       for (int b = split_b ? half : 0; b < p.MB; b += split_b ? 2 : 1) {
@@ -960,13 +1007,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int64_t pix0 = TCONV ? (int64_t(tl.nb) * p.ho + yy * p.tconv_s) * p.wo + xx * p.tconv_s
                                    : (int64_t(tl.nb) * p.ho + yy) * p.wo + xx;
         const uint32_t colb = lane_base + uint32_t(ab * ACC_COLS + b * p.n_tile);
+        EPI_T(7 + (b >> 1));
         for (int ri = split_b ? 0 : half; ri < nr; ri += split_b ? 1 : 2) {
-          const int4 rn = rt[ri];  // (first group, length, o0, tap dy << 16 | dx)
+          // (first group, length, o0, tap dy << 16 | dx)
+          const int4 rn = TCONV ? rt[ri] : make_int4(0, min(p.n_tile, p.n_gemm - jt) >> 5, jt, 0);
           const int64_t opix = TCONV ? pix0 + (rn.w >> 16) * p.wo + (rn.w & 0xFFFF) : pix0;
           uint32_t w8[8];
 #pragma unroll
           for (int rr = 0; rr < 8; ++rr) w8[rr] = 0u;
           const uint32_t col0 = colb + uint32_t(rn.x * 32);
+#ifdef ABL_NO_EPI
+          if (true) {
+          } else
+#endif
           if (p.acc == nullptr) {
             // two groups per TMEM load, one SHF per column to pack the signs
 #pragma unroll
@@ -974,15 +1027,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (rr < rn.y) {
                 if (rr + 1 < rn.y) {
                   uint32_t v[64];
-#ifdef MBU_TIMELINE
-                  if (blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64 && b < 4 && rr < 4)
-                    g_epi[it * 16 + b * 4 + (rr >> 1) * 2] = clock64();
-#endif
                   tmem_ld64(col0 + uint32_t(rr * 32), v);
-#ifdef MBU_TIMELINE
-                  if (blockIdx.x == 0 && warp == 0 && lane == 0 && it < 64 && b < 4 && rr < 4)
-                    g_epi[it * 16 + b * 4 + (rr >> 1) * 2 + 1] = clock64();
-#endif
                   w8[rr] = pack_nonneg<0>(v);
                   w8[rr + 1] = pack_nonneg<32>(v);
                 } else {
@@ -1045,8 +1090,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+      EPI_T(10);
       // buffer drained: re-arm it with the bias of the tile that reuses it
       init_buffer(t + p.nbuf * gridDim.x, ab);
+      EPI_T(11);
 #ifdef MBU_TIMELINE
       if (blockIdx.x == 0 && lane == 0 && it < 64 && warp == 0) {
         g_timeline[it * 12 + 4] = te0;
@@ -1299,7 +1346,7 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
       }
       slab_of[nt] = found;
     }
-    if (slabs_ok && slabs.size() <= 16384) {
+    if (slabs_ok && slabs.size() <= size_t(MBU_FP4_SLAB_CAP)) {
       MBU_TRY(check_cuda(cudaMalloc(&cv->d_b4, b4.size()), "alloc fp4 weights"));
       MBU_TRY(check_cuda(cudaMemcpy(cv->d_b4, b4.data(), b4.size(), cudaMemcpyHostToDevice), "upload fp4 weights"));
       MBU_TRY(check_cuda(cudaMalloc(&cv->d_chunk_pair, pairs.size() * 4), "alloc chunk pairs"));
@@ -1406,8 +1453,8 @@ static int launch_tc_impl(const tc::Params &p, const CUtensorMap &xmap, int grid
     {
       unsigned long long e[64 * 16];
       cudaMemcpyFromSymbol(e, tc::g_epi, sizeof(e));
-      for (int i = 2; i < 5; ++i) {
-        fprintf(stderr, "  epi it %d:", i);
+      for (int i = 2; i < 8; ++i) {
+        fprintf(stderr, "  mma it %d (waitE %lld got %lld):", i, (long long)(h[i * 12] - b0), (long long)(h[i * 12 + 1] - b0));
         for (int k = 0; k < 16; ++k) fprintf(stderr, " %lld", (long long)(e[i * 16 + k] ? e[i * 16 + k] - h[0] : 0));
         fprintf(stderr, "\n");
       }
@@ -1424,8 +1471,26 @@ static int launch_tc_impl(const tc::Params &p, const CUtensorMap &xmap, int grid
   return check_launch("conv_tc_kernel");
 }
 
+// kNoFit: the FP4 shared-memory layout (bias slabs + stages) does not fit;
+// the caller falls back to kind::i8 for this geometry
+constexpr int kNoFit = -1;
+static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
+                               uint64_t *bits, int out_stride, int out_offset, cudaStream_t st, bool fp4);
 int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
                    uint64_t *bits, int out_stride, int out_offset, cudaStream_t st) {
+  // 3x3 layers run kind::mxf4 (e2m1) when the uniform block-scale columns fit
+  // next to the accumulators (MB * n_tile <= 248); MBU_OPT_CONV_I8 forces kind::i8
+  const bool fp4 = cv->fp4_ok && !g_force_conv_i8 && tc::FP4_COLS / cv->n_tile >= 1;
+  if (fp4) {
+    const int r = launch_conv_tc_kind(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, true);
+    if (r != kNoFit) return r;
+  }
+  const int r = launch_conv_tc_kind(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, false);
+  return r == kNoFit ? fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv stage does not fit in shared memory") : r;
+}
+
+static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
+                               uint64_t *bits, int out_stride, int out_offset, cudaStream_t st, bool fp4) {
   tc::Params p{};
   p.x32 = reinterpret_cast<const uint32_t *>(x.base);
   p.n = x.n;
@@ -1439,9 +1504,6 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   p.halo = cv->taps == 9 ? 1 : 0;
   p.n_tile = cv->n_tile;
   p.n_tiles = cv->n_tiles;
-  // 3x3 layers run kind::mxf4 (e2m1) when the uniform block-scale columns fit
-  // next to the accumulators (MB * n_tile <= 248); MBU_OPT_CONV_I8 forces kind::i8
-  const bool fp4 = cv->fp4_ok && !g_force_conv_i8 && tc::FP4_COLS / cv->n_tile >= 1;
   // long-K FP4 layers (>= 4 K stages) trade the second accumulator for a
   // taller tile (one buffer of up to 504 columns): each weight stage then
   // feeds up to 3 (N = 128) or 7 (N = 64) pixel blocks, cutting the weight
@@ -1512,7 +1574,7 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   p.b_resident = b_all + 3 * size_t(p.a_stage_bytes) <= budget;
   const size_t stage = size_t(p.a_stage_bytes) + (p.b_resident ? 0 : p.b_stage_bytes);
   int stages = int((budget - (p.b_resident ? b_all : 0)) / stage);
-  if (stages < 2) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv stage does not fit in shared memory");
+  if (stages < 2) return kNoFit;
   p.stages = std::min(stages, tc::MAX_STAGES);
   size_t off = tc::SMEM_HEADER + size_t(p.stages) * p.a_stage_bytes;
   p.off_b = uint32_t(off);
@@ -1576,7 +1638,7 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   p.rt_magic = magic(p.row_tiles);
   const int grid = int(std::min<int64_t>(tiles, num_sms()));
   const size_t smem = std::max<size_t>(smem_total, tc::MIN_SMEM);
-  if (smem > 227 * 1024) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv shared memory layout overflow");
+  if (smem > 227 * 1024) return kNoFit;
   if (cv->transposed) return launch_tc_impl<1, true, tc::LA_TAP1, 4, false>(p, xmap, grid, smem, st);
   if (fp4) return launch_tc_impl<9, false, tc::LA_CONV3, 2, true>(p, xmap, grid, smem, st);
   if (cv->taps == 9) return launch_tc_impl<9, false, tc::LA_CONV3, 1, false>(p, xmap, grid, smem, st);

@@ -24,7 +24,7 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 // a: [128][32 B] row-major packed e2m1 (element k of row r in byte r*32 + k/2, nibble k%2)
 // b: [N][32 B]; out: [128][N] floats
 __global__ void fp4_mma(const uint8_t *a, const uint8_t *b, int n, int reps, int timing, float *out,
-                        unsigned long long *clk, int sfc, uint32_t sfa_val) {
+                        unsigned long long *clk, int sfc, uint32_t sfa_val, int aoff = 0) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar;
@@ -64,7 +64,7 @@ __global__ void fp4_mma(const uint8_t *a, const uint8_t *b, int n, int reps, int
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   if (threadIdx.x == 0) {
-    const uint64_t ad = umma_desc(smem_u32(smem), 128 * 16, 128);
+    const uint64_t ad = umma_desc(smem_u32(smem) + 16u * aoff, 128 * 16, 128);
     const uint64_t bd = umma_desc(smem_u32(smem + 8192), uint32_t(n) * 16, 128);
     // block-scaled descriptor: A/B E2M1 (1), UE8M0 scales (bit 23), N, M = 128, K = 64
     const uint32_t idesc = (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (1u << 23) | (uint32_t(128 >> 4) << 24);
@@ -154,12 +154,52 @@ int main() {
         maxabs = std::max(maxabs, std::labs(s));
         if (double(out[r * n + c]) != double(s)) ++bad;
       }
+    for (int aoff : {1, 3, 8}) {
+      fp4_mma<<<sms, 128, 32 * 1024>>>(da, db, n, 4096, 1, dout, dclk, 32, 0u, aoff);
+      unsigned long long ck[148];
+      cudaMemcpy(ck, dclk, sms * 8, cudaMemcpyDeviceToHost);
+      printf("{\"bench\": \"mxf4_ss_aoff\", \"n\": %d, \"a_row_offset\": %d, \"clk_per_mma\": %.1f}\n", n, aoff,
+             double(ck[0]) / 4096);
+    }
     fp4_mma<<<sms, 128, 32 * 1024>>>(da, db, n, 4096, 1, dout, dclk, 32, 0u);
     unsigned long long clk[148];
     cudaMemcpy(clk, dclk, sms * 8, cudaMemcpyDeviceToHost);
     const double cpm = double(clk[0]) / 4096;
     printf("{\"bench\": \"mxf4_ss\", \"n\": %d, \"exact_mismatches\": %ld, \"max_abs\": %ld, \"clk_per_mma\": %.1f, "
            "\"mac_per_clk\": %.0f}\n", n, bad, maxabs, cpm, 128.0 * n * 64 / cpm);
+  }
+  // data dependence of the MMA rate: operand nibble patterns, all SMs busy
+  for (int n : {64, 128}) {
+    for (int pat = 0; pat < 4; ++pat) {
+      std::vector<uint8_t> ap(128 * 32), bp(n * 32);
+      auto nib = [&](int which) -> uint8_t {
+        switch (pat) {
+          case 0: return 0;                                      // zeros
+          case 1: return which ? enc((rand() % 3) - 1) : (rand() & 1 ? 0x2 : 0x0);  // a' in {0,1}, w in {-1,0,1}
+          case 2: return 0x2;                                    // all ones
+          default: return uint8_t(rand() & 0xF);                 // every e2m1 code
+        }
+      };
+      for (auto &x : ap) x = uint8_t(nib(0) | (nib(0) << 4));
+      for (auto &x : bp) x = uint8_t(nib(1) | (nib(1) << 4));
+      uint8_t *da, *db;
+      float *dout;
+      unsigned long long *dclk;
+      cudaMalloc(&da, ap.size());
+      cudaMalloc(&db, bp.size());
+      cudaMalloc(&dout, 128 * n * 4);
+      cudaMalloc(&dclk, 148 * 8);
+      cudaMemcpy(da, ap.data(), ap.size(), cudaMemcpyHostToDevice);
+      cudaMemcpy(db, bp.data(), bp.size(), cudaMemcpyHostToDevice);
+      fp4_mma<<<sms, 128, 32 * 1024>>>(da, db, n, 8192, 1, dout, dclk, 32, 0u);
+      unsigned long long ck[148];
+      cudaMemcpy(ck, dclk, sms * 8, cudaMemcpyDeviceToHost);
+      double mx = 0;
+      for (int i = 0; i < sms; ++i) mx = std::max(mx, double(ck[i]));
+      printf("{\"bench\": \"mxf4_data\", \"n\": %d, \"pattern\": %d, \"clk_per_mma_cta0\": %.1f, \"clk_per_mma_max\": %.1f}\n",
+             n, pat, double(ck[0]) / 8192, mx / 8192);
+      cudaFree(da); cudaFree(db); cudaFree(dout); cudaFree(dclk);
+    }
   }
   return 0;
 }
