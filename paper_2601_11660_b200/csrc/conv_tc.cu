@@ -583,6 +583,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       c.inb = 0;
 #pragma unroll
       for (int j = 0; j < PI; ++j) {
+        if (j * PROD_THREADS >= p.Q) break;  // (uniform: items past the strip do no work)
         const int q = pt + j * PROD_THREADS;
         const int rr = int(__umulhi(uint32_t(q), p.p_magic));
         const int iy = tl.y0 - p.halo + rr;
@@ -611,6 +612,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t *dst = raw + i_slot * slot_words;
 #pragma unroll
         for (int j = 0; j < PI; ++j) {
+        if (j * PROD_THREADS >= p.Q) break;  // (uniform: items past the strip do no work)
           const int q = pt + j * PROD_THREADS;
           if (q < p.Q) {
             const bool in = (ic.inb >> j) & 1;
@@ -694,6 +696,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int qbox = p.raw_rows * p.P - 1;
 #pragma unroll
         for (int j = 0; j < PI; ++j) {
+        if (j * PROD_THREADS >= p.Q) break;  // (uniform: items past the strip do no work)
           const int q = pt + j * PROD_THREADS;
           const uint32_t *px = rw + min(q, qbox) * 4;
           const uint32_t lj = ((ec.inb >> j) & 1) ? lut : 0u;  // out of bounds -> 0
@@ -710,6 +713,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (p.u8_act) {
 #pragma unroll
           for (int j = 0; j < PI; ++j) {
+        if (j * PROD_THREADS >= p.Q) break;  // (uniform: items past the strip do no work)
             const int q = pt + j * PROD_THREADS;
             const uint32_t b = rw[min(q, qmax)];
             const uint32_t v0 = spread4(b & 0xF), v1 = spread4((b >> 4) & 0xF), v2 = spread4((b >> 8) & 0xF),
@@ -723,6 +727,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         } else {
 #pragma unroll
           for (int j = 0; j < PI; ++j) {
+        if (j * PROD_THREADS >= p.Q) break;  // (uniform: items past the strip do no work)
             const int q = pt + j * PROD_THREADS;
             const uint32_t b = rw[min(q, qmax)];
             const bool in = (ec.inb >> j) & 1;
@@ -740,6 +745,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       } else {
 #pragma unroll
         for (int j = 0; j < PI; ++j) {
+        if (j * PROD_THREADS >= p.Q) break;  // (uniform: items past the strip do no work)
           const int q = pt + j * PROD_THREADS;
           if (q < p.Q) {
 #pragma unroll
