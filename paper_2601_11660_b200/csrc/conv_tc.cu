@@ -399,16 +399,16 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
                : "memory");
 }
 
-// 32 activation bits -> 32 e2m1 lanes (16 B): each 2-bit field picks one byte
-// of `lut` (u8 mode: {0, 1.0}; s8 mode: {-1.0, +1.0}), lane 2j in the low nibble
-__device__ __forceinline__ uint32_t fp4_sel(uint32_t v) {  // byte b of a 16-bit slot -> 4 selector nibbles
-  v = (v & 0x000F000Fu) | ((v << 4) & 0x0F000F00u);
-  return (v & 0x03030303u) | ((v << 2) & 0x30303030u);
-}
-__device__ __forceinline__ uint4 fp4x32(uint32_t w, uint32_t lut) {
-  const uint32_t s0 = fp4_sel(__byte_perm(w, 0u, 0x4140)), s1 = fp4_sel(__byte_perm(w, 0u, 0x4342));
-  return make_uint4(__byte_perm(lut, 0u, s0), __byte_perm(lut, 0u, s0 >> 16), __byte_perm(lut, 0u, s1),
-                    __byte_perm(lut, 0u, s1 >> 16));
+// 32 activation bits -> 32 e2m1 lanes (16 B) in the K order the weights are
+// packed in (prepare_conv_tc, fp4_k_pos): lane i = m + 4n of the chunk lands in
+// word m, nibble n, so every word is one shift and one mask of the input.
+// u8 mode (neg_one padding): bit -> 1.0 (0x2) / 0; s8 mode (zero padding):
+// bit -> +1.0 / -1.0 (0xA); keep = 0 (out of bounds) -> all lanes 0.
+__device__ __forceinline__ uint4 fp4x32(uint32_t w, uint32_t keep, bool s8) {
+  const uint32_t one = 0x22222222u & keep;
+  if (!s8) return make_uint4((w << 1) & one, w & one, (w >> 1) & one, (w >> 2) & one);
+  const uint32_t nw = ~w, sg = 0x88888888u & keep;
+  return make_uint4(one | ((nw << 3) & sg), one | ((nw << 2) & sg), one | ((nw << 1) & sg), one | (nw & sg));
 }
 
 struct Tile {
@@ -692,15 +692,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
         // two 32-lane chunks -> one K = 64 e2m1 row: chunk c fills core-matrix column c
         // raw box: 16 B (a 128-lane block) per strip pixel, pixels row-major
-        const uint32_t lut = p.u8_act ? 0x22200200u : 0x222AA2AAu;
+        const bool s8 = !p.u8_act;
         const int qbox = p.raw_rows * p.P - 1;
 #pragma unroll
         for (int j = 0; j < PI; ++j) {
         if (j * PROD_THREADS >= p.Q) break;  // (uniform: items past the strip do no work)
           const int q = pt + j * PROD_THREADS;
           const uint32_t *px = rw + min(q, qbox) * 4;
-          const uint32_t lj = ((ec.inb >> j) & 1) ? lut : 0u;  // out of bounds -> 0
-          const uint4 e0 = fp4x32(px[ca], lj), e1 = fp4x32(px[cb], lj);
+          const uint32_t keep = ((ec.inb >> j) & 1) ? ~0u : 0u;  // out of bounds -> 0
+          const uint4 e0 = fp4x32(px[ca], keep, s8), e1 = fp4x32(px[cb], keep, s8);
           if (q < p.Q) {
             const uint32_t a0 = a_st + q * 16;
             sts128(a0, e0.x, e0.y, e0.z, e0.w);
@@ -1273,7 +1273,7 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
                      "upload column bias"));
   // FP4 (kind::mxf4) operand for 3x3 layers: chunk pairs share one K = 64
   // row (pair p = chunks 2p, 2p+1; an odd count gets a zero-weight dummy),
-  // weights as e2m1 {-1, 0, +1} nibbles, lane 2i in the low nibble
+  // weights as e2m1 {-1, 0, +1} nibbles; lane i of a chunk at K position 8 (i % 4) + i / 4
   cv->fp4_ok = 0;
   if (conv3) {
     // pairs never straddle a 128-lane block (one TMA box per stage): pair the
@@ -1310,7 +1310,8 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
               if (ci < 0) continue;  // dummy chunk: zero weights
               for (int i = 0; i < 32; ++i) {
                 const int v = wval(j, tap, 32 * chunk_word[ci] + i);
-                dst[i / 2] |= uint8_t(e2m1(col_neg[j] ? -v : v) << (4 * (i & 1)));
+                const int kp = 8 * (i % 4) + i / 4;  // K position of lane i (the producers' fp4x32 order)
+                dst[kp / 2] |= uint8_t(e2m1(col_neg[j] ? -v : v) << (4 * (kp & 1)));
               }
             }
     // bias slabs: bias + 0.5 (no signed zero) = sum(lo entries) + 256 * sum(hi entries)
