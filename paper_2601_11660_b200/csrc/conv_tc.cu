@@ -56,8 +56,8 @@
 
 #include "common.cuh"
 
-// largest FP4 bias-slab set kept resident in shared memory (64 B per GEMM
-// column: 512 output channels); launch falls back to kind::i8 if a geometry
+// largest FP4 bias-slab set kept resident in shared memory (32 B per GEMM
+// column: 1024 output channels); launch falls back to kind::i8 if a geometry
 // then leaves fewer than two pipeline stages
 #ifndef MBU_FP4_SLAB_CAP
 #define MBU_FP4_SLAB_CAP 32768
@@ -138,7 +138,8 @@ struct Params {
   uint32_t off_b, off_raw, off_runs, off_ones, off_slab, off_slabmap;
   int b_resident;           // all weights resident in smem (loaded once), no B stream
   int mma_bias;             // bias enters the accumulator by an MMA (ones x bias slab)
-  uint32_t sf1, sf256;      // FP4: TMEM columns of the uniform 2^0 / 2^8 block scales
+  uint32_t sf1, sf256;      // FP4: TMEM columns of the 2^0 block scales and of the bias MMA's
+                            // A scales (2^0 for K 0-31, 2^8 for K 32-63)
   // FP4: raw activation blocks arrive by TMA (one box of 16 B x P x strip rows per stage)
   uint32_t off_rraw, rraw_bytes, rraw_box_bytes;
   int rraw_stages, raw_rows;
@@ -514,7 +515,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     runs_s[nt * 9] = make_int4(r, 0, 0, 0);
   }
   if (p.mma_bias) {  // ones slab (16 x 1, 16 x 127 per row) + bias slabs, read by the tensor core
-    // (FP4: every entry e2m1 1.0; bias = sum(lo) + 256 * sum(hi), two slabs per N tile)
+    // (FP4: every entry e2m1 1.0; bias = sum(lo) + 256 * sum(hi), one K = 64 slab per N tile)
     uint4 *ones = reinterpret_cast<uint4 *>(smem + p.off_ones);
     for (int i = threadIdx.x; i < 256; i += blockDim.x)
       ones[i] = FP4 ? make_uint4(0x22222222u, 0x22222222u, 0x22222222u, 0x22222222u)
@@ -522,7 +523,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                               : make_uint4(0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu);
     uint4 *slab = reinterpret_cast<uint4 *>(smem + p.off_slab);
     const uint4 *src = reinterpret_cast<const uint4 *>(p.bias_slab);
-    for (int i = threadIdx.x; i < p.n_slabs * p.n_tile * (FP4 ? 4 : 2); i += blockDim.x) slab[i] = src[i];
+    for (int i = threadIdx.x; i < p.n_slabs * p.n_tile * 2; i += blockDim.x) slab[i] = src[i];
     int32_t *smap = reinterpret_cast<int32_t *>(smem + p.off_slabmap);
     for (int i = threadIdx.x; i < p.n_tiles; i += blockDim.x) smap[i] = p.slab_of_nt[i];
     fence_proxy_async();
@@ -546,7 +547,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int c = 0; c < 4; ++c) {
         asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(lq + p.sf1 + c), "r"(0x7F7F7F7Fu)
                      : "memory");
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(lq + p.sf256 + c), "r"(0x87878787u)
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(lq + p.sf256 + c), "r"(0x7F7F877Fu)
                      : "memory");
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -825,13 +826,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
         tc_fence_after();
         const uint32_t d0 = tmem + uint32_t(ab * ACC_COLS);
-        if (FP4 && p.mma_bias) {  // bias = lo (scale 1) + 256 * hi (A scale 2^8)
-          const uint64_t sd = slab_desc0 + uint64_t(slab) * uint64_t(p.n_tile * 4);
-          for (int b = 0; b < p.MB; ++b) {
-            umma1_fp4(d0 + uint32_t(b * p.n_tile), ones_desc, sd, p.idesc, tmem + p.sf1, tmem + p.sf1, 0u);
-            umma1_fp4(d0 + uint32_t(b * p.n_tile), ones_desc, sd + uint64_t(p.n_tile * 2), p.idesc,
-                      tmem + p.sf256, tmem + p.sf1, 1u);
-          }
+        if (FP4 && p.mma_bias) {  // bias = lo (K 0-31, A scale 1) + 256 * hi (K 32-63, A scale 2^8)
+          const uint64_t sd = slab_desc0 + uint64_t(slab) * uint64_t(p.n_tile * 2);
+          for (int b = 0; b < p.MB; ++b)
+            umma1_fp4(d0 + uint32_t(b * p.n_tile), ones_desc, sd, p.idesc, tmem + p.sf256, tmem + p.sf1, 0u);
         } else if (p.mma_bias) {
           const uint64_t sd = slab_desc0 + uint64_t(slab) * uint64_t(p.n_tile * 2);
           for (int b = 0; b < p.MB; ++b) umma1_i8_first(d0 + uint32_t(b * p.n_tile), ones_desc, sd, p.idesc);
@@ -1314,8 +1312,9 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
                 dst[kp / 2] |= uint8_t(e2m1(col_neg[j] ? -v : v) << (4 * (kp & 1)));
               }
             }
-    // bias slabs: bias + 0.5 (no signed zero) = sum(lo entries) + 256 * sum(hi entries)
-    const size_t sb = size_t(n_tile) * 64;  // lo + hi slabs of one N tile
+    // bias slabs: bias + 0.5 (no signed zero) = sum(lo entries, K 0-31) +
+    // 256 * sum(hi entries, K 32-63); the bias MMA's A block scales are 2^0 / 2^8
+    const size_t sb = size_t(n_tile) * 32;  // one K = 64 slab per N tile
     std::vector<uint8_t> slabs;
     std::vector<int32_t> slab_of(n_tiles);
     bool slabs_ok = true;
@@ -1327,17 +1326,15 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
         const double lo = double(bias - 256 * hi) + 0.5;
         for (int part = 0; part < 2; ++part) {
           const double v = part == 0 ? lo : double(hi);
-          // entries e = 0..63 of column n: khalf e / 32, byte (e % 32) / 2, nibble e % 2
+          // entries e = 0..31 of column n in K half `part`: byte e / 2, nibble e % 2
           static const double mag[7] = {6, 4, 3, 2, 1.5, 1, 0.5};
           static const uint8_t code[7] = {7, 6, 5, 4, 3, 2, 1};
           const uint8_t sg = v < 0 ? 0x8 : 0x0;
           double r = std::fabs(v);
           int e = 0;
           for (int m = 0; m < 7; ++m)
-            while (r >= mag[m] && e < 64) {
-              uint8_t *slab = sl.data() + size_t(part) * n_tile * 32;
-              slab[size_t(e / 32) * n_tile * 16 + size_t(n) * 16 + (e % 32) / 2] |=
-                  uint8_t((code[m] | sg) << (4 * (e & 1)));
+            while (r >= mag[m] && e < 32) {
+              sl[size_t(part) * n_tile * 16 + size_t(n) * 16 + e / 2] |= uint8_t((code[m] | sg) << (4 * (e & 1)));
               r -= mag[m];
               ++e;
             }
@@ -1574,7 +1571,7 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   const size_t raw_bytes = fp4 ? size_t(p.rraw_stages) * p.rraw_bytes : size_t(raw_stages) * Q * cps * 4;
   const size_t runs_bytes = size_t(cv->n_tiles) * 9 * 16 + size_t(cv->n_tiles) * cv->n_tile * 4;
   const int n_slabs = fp4 ? cv->n_slabs4 : cv->n_slabs;
-  const size_t slab_bytes = size_t(n_slabs) * cv->n_tile * (fp4 ? 64 : 32);
+  const size_t slab_bytes = size_t(n_slabs) * cv->n_tile * 32;
   const size_t bias_bytes = n_slabs ? 4096 + slab_bytes + 1024 : 0;
   const size_t budget = 227 * 1024 - tc::SMEM_HEADER - raw_bytes - runs_bytes - bias_bytes - 1024 - 128;
   const size_t b_all = size_t(cv->n_tiles) * p.ks * p.b_stage_bytes;

@@ -279,6 +279,33 @@ int main() {
       }
     cudaFree(dclk);
   }
+  // block-scale layout: which byte of the A scale word scales which 32-wide K block
+  {
+    const int n = 64;
+    uint8_t *da, *db;
+    float *dout;
+    unsigned long long *dclk;
+    cudaMalloc(&da, 128 * 32);
+    cudaMalloc(&db, n * 32);
+    cudaMalloc(&dout, 128 * n * 4);
+    cudaMalloc(&dclk, 148 * 8);
+    std::vector<uint8_t> bp(n * 32, 0x22);  // B: every element 1.0
+    cudaMemcpy(db, bp.data(), bp.size(), cudaMemcpyHostToDevice);
+    for (int kb = 0; kb < 2; ++kb) {
+      std::vector<uint8_t> ap(128 * 32, 0);
+      for (int r = 0; r < 128; ++r)
+        for (int byte = 16 * kb; byte < 16 * kb + 16; ++byte) ap[r * 32 + byte] = 0x22;  // K block kb = 1.0
+      cudaMemcpy(da, ap.data(), ap.size(), cudaMemcpyHostToDevice);
+      for (uint32_t sv : {0x7F7F7F87u, 0x7F7F877Fu, 0x7F877F7Fu, 0x877F7F7Fu}) {
+        fp4_mma<<<1, 128, 32 * 1024>>>(da, db, n, 1, 0, dout, dclk, 4, sv);
+        std::vector<float> o(128 * n);
+        cudaMemcpy(o.data(), dout, o.size() * 4, cudaMemcpyDeviceToHost);
+        printf("{\"probe\": \"sf_layout\", \"a_ones_in_kblock\": %d, \"sfa_word\": \"0x%08X\", \"d00\": %g, \"d_127_63\": %g}\n",
+               kb, sv, o[0], o[127 * n + 63]);
+      }
+    }
+    cudaFree(da); cudaFree(db); cudaFree(dout); cudaFree(dclk);
+  }
   // data dependence of the MMA rate: operand nibble patterns, all SMs busy
   for (int n : {64, 128}) {
     for (int pat = 0; pat < 4; ++pat) {
