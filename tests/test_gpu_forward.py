@@ -218,3 +218,22 @@ def test_multiclass_head_and_class_map(cuda, classes):
     assert got.dtype == np.uint8 and np.array_equal(got, np.argmax(lg, axis=-1))
     gd = mb.argmax_classes(torch.from_numpy(lg).to(cuda))
     assert gd.is_cuda and np.array_equal(gd.cpu().numpy(), np.argmax(lg, axis=-1))
+
+
+def test_wide_layers_fp4_cap_and_i8_fallback(cuda):
+    """1024- and 1056-channel layers: FP4 bias slabs at the 32 KB cap, and past it
+    (kind::i8 fallback); fast (bits only) and trace forwards against the dense oracle."""
+    cfg = mb.UNetConfig(height=64, width=64, encoder_channels=(64, 128, 1024, 1056),
+                        tconv_channels=(256, 128, 64, 32), decoder_channels=(256, 128, 64, 32))
+    rng = np.random.default_rng(17)
+    bundle = mb.live_bundle(cfg, rng)
+    model = mb.build(cfg, bundle)
+    image = rng.random((2, 64, 64, 3))
+    fast = mb.forward(model, image)
+    traced = mb.forward(model, image, trace=True)
+    ref = dense.ref_forward(cfg, mb.dense_records(mb.quantize_bundle(bundle, cfg), cfg), image)
+    assert np.array_equal(fast.mask, ref["mask"])
+    assert np.array_equal(traced.mask, ref["mask"])
+    assert np.array_equal(fast.logits, traced.logits)
+    for name in ("down-C3.a", "down-C4.a", "down-C4.b"):
+        assert np.array_equal(traced.trace[name]["acc"], ref[name]["acc"]), name
