@@ -177,6 +177,21 @@ __global__ void fp4_mma_strip(int n, int q, int reps, int noise, unsigned long l
                    : "=r"(ok) : "r"(smem_u32(&bar)));
     clk[blockIdx.x] = clock64() - t0;
     stop = 1;
+  } else if (warp >= 4 && noise == 2) {
+    // tcgen05.ld of the upper TMEM half (columns 256..479) by warps 4..15, until the MMAs finish
+    const uint32_t lq = tmem + (uint32_t((warp & 3) * 32) << 16) + 256u + uint32_t((warp >> 2) - 1) * 64u;
+    uint32_t acc = 0;
+    while (!stop) {
+      uint32_t v[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(lq & ~0u));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      for (int i = 0; i < 16; ++i) acc += v[i];
+    }
+    if (acc == 0x12345678u) clk[gridDim.x + blockIdx.x] = acc;
   } else if (warp >= 4 && noise) {
     // 16-B stores over a 32 KB scratch region (bandwidth hog), until the MMAs finish
     uint4 *sc = reinterpret_cast<uint4 *>(scratch);
@@ -266,10 +281,10 @@ int main() {
   cudaFuncSetAttribute(fp4_mma_strip, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   {
     unsigned long long *dclk;
-    cudaMalloc(&dclk, 148 * 8);
+    cudaMalloc(&dclk, 2 * 148 * 8);
     for (int n : {64, 128})
-      for (int mode : {0, 1, 2})
-      for (int noise : {0, 1}) {
+      for (int mode : {2})
+      for (int noise : {0, 1, 2}) {
         fp4_mma_strip<<<sms, 512, 200 * 1024>>>(n, 656, 27 * 300, noise, dclk, mode);
         unsigned long long ck[148];
         cudaError_t e = cudaMemcpy(ck, dclk, sms * 8, cudaMemcpyDeviceToHost);
