@@ -154,6 +154,24 @@ int mbu_decode_raster(const void *raster, int64_t count, int bytes_per_sample, i
                       double *out, void *stream);
 
 /* ------------------------------------------------------------------ */
+/* Build-time quantization (quantizer.py:254-309 quantize_bundle)      */
+/* ------------------------------------------------------------------ */
+/* Dense int8 weights from float32 (device pointers, n elements):
+ * binary != 0: sign(w) with sign(0) = +1 (binarize_values, quantizer.py:105-110);
+ * else w > delta -> +1, w < -delta -> -1, 0 otherwise (ternarize_values,
+ * quantizer.py:86-102; delta = t * mean|w| computed by the caller). */
+int mbu_quantize_weights(const float *w, int64_t n, int binary, double delta, int8_t *out,
+                         void *stream);
+/* fuse_bn_sign (layers.py:455-505): per-channel int32 thresholds and codes
+ * (DIR_GE 0, DIR_LE 1, CONST_NEG 2, CONST_POS 3) of the float64 predicate
+ * gamma*((acc + bias) - mean)/sqrt(var + eps) + beta >= 0. Device pointers;
+ * bias may be NULL. Validation of the parameters (finite, var >= 0) is the
+ * caller's (ALPHABET for eps <= 0 here). */
+int mbu_fuse_bn_sign(const double *gamma, const double *beta, const double *mean,
+                     const double *var, double eps, const double *bias, int c,
+                     int32_t *thresholds, uint8_t *codes, void *stream);
+
+/* ------------------------------------------------------------------ */
 /* Whole-network runner (graph.py:413-458 forward)                     */
 /* ------------------------------------------------------------------ */
 typedef struct mbu_model mbu_model;

@@ -47,6 +47,8 @@ __all__ = [
     "float_bn_sign",
     "bit_gemm",
     "xor_popcount_rows",
+    "quantize_weights",
+    "fuse_bn_sign",
 ]
 
 
@@ -382,3 +384,59 @@ def decode_raster(raster, maxval: int, *, out=None, device=None):
     with torch.cuda.device(dev):
         _lib.call("mbu_decode_raster", _ptr(r), out.numel(), bps, int(maxval), _ptr(out), _stream(dev))
     return out
+
+
+def quantize_weights(w, state: str, ternary_t: float = 0.7, *, device=None) -> np.ndarray:
+    """``ternarize_values`` / ``binarize_values`` (quantizer.py:86-110) on the
+    GPU (``mbu_quantize_weights``): dense int8 {-1, 0, +1} weights. The
+    ternary threshold ``delta = t * mean|w|`` is the host's numpy float64
+    reduction, as in the reference, so every element lands identically;
+    already-ternary tensors pass through unchanged."""
+    from .errors import ValueAlphabetError
+    from .graph import MASKED as MASKED_STATE
+    from .quantizer import _exactly
+
+    w = np.asarray(w)
+    if w.size == 0:
+        raise ShapeError(f"cannot {'ternarize' if state == MASKED_STATE else 'binarize'} an empty tensor")
+    delta = 0.0
+    if state == MASKED_STATE:
+        if ternary_t < 0:
+            raise ValueAlphabetError(f"threshold factor must be >= 0, got {ternary_t}")
+        if _exactly(w, (-1, 0, 1)):
+            return w.astype(np.int8)
+        delta = float(ternary_t * np.abs(w).mean(dtype=np.float64))
+    dev = cuda_device(device)
+    with torch.cuda.device(dev):
+        src = torch.from_numpy(np.ascontiguousarray(w, dtype=np.float32)).to(dev)
+        out = torch.empty(src.shape, dtype=torch.int8, device=dev)
+        _lib.call("mbu_quantize_weights", _ptr(src), src.numel(), 0 if state == MASKED_STATE else 1,
+                  delta, _ptr(out), _stream(dev))
+        return out.cpu().numpy()
+
+
+def fuse_bn_sign(gamma, beta, mean, var, eps, bias=None, *, device=None) -> FusedThreshold:
+    """``fuse_bn_sign`` (layers.py:455-505) on the GPU (``mbu_fuse_bn_sign``):
+    one thread per channel bisects the int32 range against the float64
+    predicate; same validation and errors as the reference."""
+    from .errors import ValueAlphabetError
+
+    gamma, beta, mean, var = (np.asarray(a, dtype=np.float64) for a in (gamma, beta, mean, var))
+    c = gamma.shape[0]
+    if not (beta.shape == mean.shape == var.shape == (c,)):
+        raise ShapeError("batchnorm vectors must share one channel axis")
+    b = np.zeros(c) if bias is None else np.asarray(bias, dtype=np.float64)
+    if b.shape != (c,):
+        raise ShapeError(f"bias shape {b.shape} != ({c},)")
+    if np.any(var < 0):
+        raise ValueAlphabetError("variance must be nonnegative")
+    if not np.isfinite(np.stack([gamma, beta, mean, var, b])).all() or not (eps > 0 and np.isfinite(eps)):
+        raise ValueAlphabetError("batchnorm parameters must be finite with eps > 0")
+    dev = cuda_device(device)
+    with torch.cuda.device(dev):
+        ts = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (gamma, beta, mean, var, b)]
+        thr = torch.empty(c, dtype=torch.int32, device=dev)
+        codes = torch.empty(c, dtype=torch.uint8, device=dev)
+        _lib.call("mbu_fuse_bn_sign", *(_ptr(t) for t in ts[:4]), float(eps), _ptr(ts[4]), c,
+                  _ptr(thr), _ptr(codes), _stream(dev))
+        return FusedThreshold(thr.cpu().numpy(), codes.cpu().numpy())

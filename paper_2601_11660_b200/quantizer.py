@@ -112,8 +112,21 @@ class PreparedLayer:
     threshold: FusedThreshold | None = None
 
 
-def quantize_bundle(bundle, config, ternary_t: float = DEFAULT_TERNARY_T) -> dict:
-    """Quantize every conv of ``bundle`` per the config's PrecisionMap."""
+def quantize_bundle(bundle, config, ternary_t: float = DEFAULT_TERNARY_T, *, device=None) -> dict:
+    """Quantize every conv of ``bundle`` per the config's PrecisionMap.
+
+    ``device`` (an extra): run the element-wise
+    ternarize / binarize and the per-channel ``fuse_bn_sign`` searches on that
+    CUDA device (``ops.quantize_weights`` / ``ops.fuse_bn_sign``); the result
+    is identical to the host path."""
+    if device is not None:
+        from . import ops
+
+        quant = lambda w, state: ops.quantize_weights(w, state, ternary_t, device=device)  # noqa: E731
+        fuse = lambda *bn, bias: ops.fuse_bn_sign(*bn, bias=bias, device=device)  # noqa: E731
+    else:
+        quant = lambda w, state: ternarize_values(w, ternary_t) if state == "masked" else binarize_values(w)  # noqa: E731
+        fuse = lambda *bn, bias: fuse_bn_sign(*bn, bias=bias)  # noqa: E731
     from .graph import MASKED, layer_specs
 
     out = {}
@@ -143,9 +156,9 @@ def quantize_bundle(bundle, config, ternary_t: float = DEFAULT_TERNARY_T) -> dic
                                         be.bn_tuple() if be.has_bn else None)
             continue
         state = MASKED if e.label == "stem2" else config.precision.state(e.label)
-        dense = ternarize_values(w, ternary_t) if state == MASKED else binarize_values(w)
+        dense = quant(w, state)
         bn = be.bn_tuple()
-        out[e.name] = PreparedLayer(e.name, state, dense, bias, bn, fuse_bn_sign(*bn, bias=bias))
+        out[e.name] = PreparedLayer(e.name, state, dense, bias, bn, fuse(*bn, bias=bias))
     return out
 
 
