@@ -109,6 +109,7 @@ __global__ void fp4_mma_strip(int n, int q, int reps, int noise, unsigned long l
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar2;
   __shared__ volatile int stop;
   const int warp = threadIdx.x >> 5;
   uint8_t *a = smem, *b = smem + 65536, *scratch = smem + 65536 + 65536;
@@ -117,6 +118,7 @@ __global__ void fp4_mma_strip(int n, int q, int reps, int noise, unsigned long l
   if (threadIdx.x == 0) {
     stop = 0;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar2)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("fence.proxy.async.shared::cta;");
@@ -142,7 +144,31 @@ __global__ void fp4_mma_strip(int n, int q, int reps, int noise, unsigned long l
     const uint32_t sf = tmem + 480;
     const int P = 130;
     const unsigned long long t0 = clock64();
-    if (mode == 2) {  // unrolled 9-tap walk per block, 64-bit adds only (the kernel's umma9)
+    if (mode >= 3) {  // mode 2 plus a tcgen05.commit to a second barrier after every (mode - 2) blocks
+      const uint64_t pp = P, bs = uint64_t(n) * 2;
+      const int every = mode - 2;
+      for (int i = 0; i < reps / 27; ++i)
+        for (int blk = 0; blk < 3; ++blk) {
+          const uint64_t ac = umma_desc(smem_u32(a) + 16u * ((blk + 1) * P + 1), uint32_t(q) * 16, 128);
+          const uint64_t b0 = umma_desc(smem_u32(b), uint32_t(n) * 16, 128);
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const uint64_t ad = ac + (uint64_t(tap / 3) - 1) * pp + uint64_t(tap % 3) - 1;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n\t}" ::"r"(
+                    tmem + uint32_t(blk * n)),
+                "l"(ad), "l"(b0 + uint64_t(tap) * bs), "r"(idesc), "r"(1), "r"(sf));
+          }
+          if (mode < 6 && (i * 3 + blk) % every == every - 1)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                smem_u32(&bar2)));
+          if (mode == 7 && (i * 3 + blk) % 5 == 9) clk[gridDim.x] = i;  // control flow, no commit
+        }
+        if (mode == 6)  // one commit per 27 MMAs, no per-block test
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+              smem_u32(&bar2)));
+    } else if (mode == 2) {  // unrolled 9-tap walk per block, 64-bit adds only (the kernel's umma9)
       const uint64_t pp = P, bs = uint64_t(n) * 2;
       for (int i = 0; i < reps / 27; ++i)
         for (int blk = 0; blk < 3; ++blk) {
@@ -177,6 +203,13 @@ __global__ void fp4_mma_strip(int n, int q, int reps, int noise, unsigned long l
                    : "=r"(ok) : "r"(smem_u32(&bar)));
     clk[blockIdx.x] = clock64() - t0;
     stop = 1;
+  } else if (warp >= 4 && noise == 3) {
+    // warps 4..15 parked in try_wait (suspend hint, as the kernel's mbar_wait) on a barrier
+    // whose phase completes only when the MMAs are done
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{\n\t.reg .pred q;\n\tmbarrier.try_wait.parity.shared::cta.b64 q, [%1], 0, %2;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+                   : "=r"(ok) : "r"(smem_u32(&bar)), "r"(0x989680));
   } else if (warp >= 4 && noise == 2) {
     // tcgen05.ld of the upper TMEM half (columns 256..479) by warps 4..15, until the MMAs finish
     const uint32_t lq = tmem + (uint32_t((warp & 3) * 32) << 16) + 256u + uint32_t((warp >> 2) - 1) * 64u;
@@ -283,8 +316,8 @@ int main() {
     unsigned long long *dclk;
     cudaMalloc(&dclk, 2 * 148 * 8);
     for (int n : {64, 128})
-      for (int mode : {2})
-      for (int noise : {0, 1, 2}) {
+      for (int mode : {2, 3, 6, 7})
+      for (int noise : {0}) {
         fp4_mma_strip<<<sms, 512, 200 * 1024>>>(n, 656, 27 * 300, noise, dclk, mode);
         unsigned long long ck[148];
         cudaError_t e = cudaMemcpy(ck, dclk, sms * 8, cudaMemcpyDeviceToHost);
