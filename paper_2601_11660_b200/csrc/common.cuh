@@ -100,6 +100,7 @@ struct mbu_conv {
   // FP4 (kind::mxf4) operand of 3x3 layers: chunk pairs, e2m1 weights, slabs
   int fp4_ok = 0;
   int kp = 0;                    // chunk pairs
+  int pair2_ok = 0;  // FP4: pairs 2j, 2j+1 share a 128-lane block (two pairs per stage)
   int pair_consec = 0;           // every pair = two consecutive words, even-aligned
   int32_t *d_chunk_pair = nullptr;
   int8_t *d_b4 = nullptr;

@@ -122,6 +122,7 @@ struct Params {
   int ks;                   // K stages per tile = kc / cps
   int vec;                  // raw chunks of a stage are consecutive, aligned words
   uint32_t a_chunk_bytes;   // A bytes of one chunk inside a stage (Q * 32)
+  uint32_t b_pair_bytes;    // FP4 with CPS = 4: weight bytes of one chunk pair (9 taps x n_tile x 32 B)
   const int32_t *chunk_word;
   const int8_t *b;
   int n_tile;
@@ -663,8 +664,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int g = 0; g < LA; ++g) issue();
     }
     for (int g = 0; g < n_stages_total; ++g) {
-      // FP4: this stage's chunk pair (read before the waits, off the expansion's path)
-      const int ca = FP4 ? chunk_s[2 * e_k] & 3 : 0, cb = FP4 ? chunk_s[2 * e_k + 1] & 3 : 0;
+      // FP4: this stage's chunk pair(s) (read before the waits, off the expansion's path);
+      // CPS = 4 stages hold both pairs of one 128-lane block
+      constexpr int PPS = FP4 ? CPS / 2 : 1;
+      const int ca = FP4 ? chunk_s[2 * PPS * e_k] & 3 : 0, cb = FP4 ? chunk_s[2 * PPS * e_k + 1] & 3 : 0;
+      const int ca2 = PPS > 1 ? chunk_s[2 * PPS * e_k + 2] & 3 : 0, cb2 = PPS > 1 ? chunk_s[2 * PPS * e_k + 3] & 3 : 0;
       if constexpr (!FP4) {
         issue();
         asm volatile("cp.async.wait_group %0;" ::"n"(LA) : "memory");  // group g landed
@@ -706,6 +710,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t a0 = a_st + q * 16;
             sts128(a0, e0.x, e0.y, e0.z, e0.w);
             sts128(a0 + p.Q * 16, e1.x, e1.y, e1.z, e1.w);
+            if constexpr (PPS > 1) {  // the block's second pair: the stage's next A region
+              const uint4 e2 = fp4x32(px[ca2], keep, s8), e3 = fp4x32(px[cb2], keep, s8);
+              sts128(a0 + p.a_chunk_bytes, e2.x, e2.y, e2.z, e2.w);
+              sts128(a0 + p.a_chunk_bytes + p.Q * 16, e3.x, e3.y, e3.z, e3.w);
+            }
           }
         }
       } else if constexpr (cps == 1) {
@@ -857,6 +866,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int b = 0; b < p.MB; ++b) {
               umma9_fp4(d0 + uint32_t(b * p.n_tile), a_s + uint64_t(block_q0(p, b)), b_s, pp, bs, p.idesc,
                         tmem + p.sf1);
+              if constexpr (CPS == 4)
+                umma9_fp4(d0 + uint32_t(b * p.n_tile), a_s + uint64_t(p.a_chunk_bytes >> 4) + uint64_t(block_q0(p, b)),
+                          b_s + uint64_t(p.b_pair_bytes >> 4), pp, bs, p.idesc, tmem + p.sf1);
               if (k == 0) MMA_T(2 + b);
             }
           } else if (TAPS == 9) {
@@ -912,7 +924,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             asm volatile(
                 "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
                 "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(smem + p.off_rraw + rs * p.rraw_bytes)),
-                "l"(&xmap), "r"(p.x_off32 + 4 * (chunk_s[2 * k] >> 2)), "r"(tl.x0 - p.halo), "r"(tl.y0 - p.halo),
+                "l"(&xmap), "r"(p.x_off32 + 4 * (chunk_s[2 * (FP4 ? CPS / 2 : 1) * k] >> 2)), "r"(tl.x0 - p.halo), "r"(tl.y0 - p.halo),
                 "r"(tl.nb), "r"(rb)
                 : "memory");
             if (++rs == p.rraw_stages) {
@@ -1366,6 +1378,10 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
       cv->n_slabs4 = int(slabs.size() / sb);
       cv->kp = kp;
       cv->pair_consec = consec ? 1 : 0;
+      // pairs 2j, 2j+1 read the same 128-lane block: one stage can take both
+      bool two = kp % 2 == 0;
+      for (int q = 0; two && q < kp; q += 2) two = (pairs[2 * q] >> 2) == (pairs[2 * q + 2] >> 2);
+      cv->pair2_ok = two ? 1 : 0;
       cv->fp4_ok = 1;
     }
   }
@@ -1479,22 +1495,26 @@ static int launch_tc_impl(const tc::Params &p, const CUtensorMap &xmap, int grid
 // the caller falls back to kind::i8 for this geometry
 constexpr int kNoFit = -1;
 static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
-                               uint64_t *bits, int out_stride, int out_offset, cudaStream_t st, bool fp4);
+                               uint64_t *bits, int out_stride, int out_offset, cudaStream_t st, bool fp4,
+                               bool allow_pps2);
 int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
                    uint64_t *bits, int out_stride, int out_offset, cudaStream_t st) {
   // 3x3 layers run kind::mxf4 (e2m1) when the uniform block-scale columns fit
   // next to the accumulators (MB * n_tile <= 248); MBU_OPT_CONV_I8 forces kind::i8
   const bool fp4 = cv->fp4_ok && !g_force_conv_i8 && tc::FP4_COLS / cv->n_tile >= 1;
   if (fp4) {
-    const int r = launch_conv_tc_kind(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, true);
-    if (r != kNoFit) return r;
+    for (int allow = 1; allow >= 0; --allow) {  // two pairs per stage if that layout fits, else one
+      const int r = launch_conv_tc_kind(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, true, allow != 0);
+      if (r != kNoFit) return r;
+    }
   }
-  const int r = launch_conv_tc_kind(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, false);
+  const int r = launch_conv_tc_kind(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, false, false);
   return r == kNoFit ? fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv stage does not fit in shared memory") : r;
 }
 
 static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
-                               uint64_t *bits, int out_stride, int out_offset, cudaStream_t st, bool fp4) {
+                               uint64_t *bits, int out_stride, int out_offset, cudaStream_t st, bool fp4,
+                               bool allow_pps2) {
   tc::Params p{};
   p.x32 = reinterpret_cast<const uint32_t *>(x.base);
   p.n = x.n;
@@ -1541,15 +1561,20 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   p.Q = Q;
   // one-tap convs pack four 32-lane chunks (a 128-lane block) into a stage;
   // FP4 3x3 stages hold a chunk pair (K = 64 e2m1 lanes in the same 32 B row)
-  const int cps = fp4 ? 2 : cv->taps == 1 ? 4 : 1;
+  // FP4 N = 128 one-block layers take both pairs of a 128-lane block per stage
+  // (one TMA box and one commit per block; measured -9% on those layers)
+  const bool pps2 = allow_pps2 && fp4 && cv->pair2_ok && cv->n_tile == 128 && p.MB == 1 &&
+                    !std::getenv("MBU_FP4_PPS1");
+  const int cps = fp4 ? (pps2 ? 4 : 2) : cv->taps == 1 ? 4 : 1;
   const int kcs = fp4 ? 2 * cv->kp : cv->kc;
   if (kcs % cps) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 one-tap conv needs whole 128-lane blocks");
   p.ks = kcs / cps;
   p.vec = fp4 ? (cv->pair_consec && p.x_stride32 % 2 == 0 && p.x_off32 % 2 == 0)
               : ((cv->chunk_consec >> (cps >> 1)) & 1) && p.x_stride32 % cps == 0 && p.x_off32 % cps == 0;
   p.a_chunk_bytes = uint32_t(Q) * 32;
-  p.a_stage_bytes = uint32_t((size_t(Q) * 32 * (fp4 ? 1 : cps) + 1023) / 1024 * 1024);
-  p.b_stage_bytes = uint32_t(cv->b_stage_bytes * (fp4 ? 1 : cps));
+  p.a_stage_bytes = uint32_t((size_t(Q) * 32 * (fp4 ? cps / 2 : cps) + 1023) / 1024 * 1024);
+  p.b_stage_bytes = uint32_t(cv->b_stage_bytes * (fp4 ? cps / 2 : cps));
+  p.b_pair_bytes = uint32_t(cv->b_stage_bytes);
   const int raw_stages = (cv->taps == 9 ? tc::LA_CONV3 : tc::LA_TAP1) + 1;
   // shared memory: [header][A stages][B stages | resident B][raw ring][runs, biases][ones][slabs][slab map]
   // (FP4: the raw ring holds TMA boxes of one 128-lane block per strip pixel)
@@ -1644,6 +1669,7 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   const size_t smem = std::max<size_t>(smem_total, tc::MIN_SMEM);
   if (smem > 227 * 1024) return kNoFit;
   if (cv->transposed) return launch_tc_impl<1, true, tc::LA_TAP1, 4, false>(p, xmap, grid, smem, st);
+  if (fp4 && cps == 4) return launch_tc_impl<9, false, tc::LA_CONV3, 4, true>(p, xmap, grid, smem, st);
   if (fp4) return launch_tc_impl<9, false, tc::LA_CONV3, 2, true>(p, xmap, grid, smem, st);
   if (cv->taps == 9) return launch_tc_impl<9, false, tc::LA_CONV3, 1, false>(p, xmap, grid, smem, st);
   return launch_tc_impl<1, false, tc::LA_TAP1, 4, false>(p, xmap, grid, smem, st);
