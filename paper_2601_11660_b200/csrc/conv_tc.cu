@@ -460,7 +460,10 @@ __device__ __forceinline__ Run run_at(const Params &p, int jt, int g, int groups
 }
 
 // ------------------------------------------------------------------ kernel
-template <int TAPS, bool TCONV, int LA, int CPS, bool FP4>
+// BLOCK_COMMIT (single-buffered long-K FP4 tiles): the last K stage commits
+// every M block on its own barrier, so the epilogue starts on block 0 while
+// the MMAs of the later blocks still run (-8% on those layers)
+template <int TAPS, bool TCONV, int LA, int CPS, bool FP4, bool BLOCK_COMMIT = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap xmap) {
   constexpr int RAW_STAGES = LA + 1;
@@ -469,7 +472,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
   uint64_t *empty = full + MAX_STAGES;
   uint64_t *acc_full = empty + MAX_STAGES;
-  uint64_t *acc_empty = acc_full + 2;
+  uint64_t *acc_empty = acc_full + 8;  // (acc_full[8]: per-block barriers under BLOCK_COMMIT)
   uint64_t *bres = acc_empty + 2;  // resident weights landed
   uint64_t *rfull = bres + 1;       // [8] FP4: raw box landed (TMA)
   uint64_t *rempty = rfull + 8;     // [8] FP4: raw box consumed (producers)
@@ -492,10 +495,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(smem_u32(&rfull[i]), 1);
       mbar_init(smem_u32(&rempty[i]), PROD_THREADS);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(smem_u32(&acc_full[i]), 1);
-      mbar_init(smem_u32(&acc_empty[i]), EPI_THREADS);
-    }
+    for (int i = 0; i < 8; ++i) mbar_init(smem_u32(&acc_full[i]), 1);
+    for (int i = 0; i < 2; ++i) mbar_init(smem_u32(&acc_empty[i]), EPI_THREADS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = threadIdx.x; i < p.kc; i += blockDim.x) chunk_s[i] = p.chunk_word[i];
@@ -869,6 +870,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if constexpr (CPS == 4)
                 umma9_fp4(d0 + uint32_t(b * p.n_tile), a_s + uint64_t(p.a_chunk_bytes >> 4) + uint64_t(block_q0(p, b)),
                           b_s + uint64_t(p.b_pair_bytes >> 4), pp, bs, p.idesc, tmem + p.sf1);
+              if constexpr (BLOCK_COMMIT) {
+                if (k == p.ks - 1) umma_commit_elect(smem_u32(&acc_full[b]));
+              }
               if (k == 0) MMA_T(2 + b);
             }
           } else if (TAPS == 9) {
@@ -888,7 +892,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ph ^= 1;
           }
         }
-        umma_commit_elect(smem_u32(&acc_full[ab]));
+        if constexpr (!BLOCK_COMMIT) umma_commit_elect(smem_u32(&acc_full[ab]));
         MMA_T(12);
 #ifdef MBU_TIMELINE
         if (blockIdx.x == 0 && lane == 0 && it < 64) {
@@ -1002,7 +1006,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #ifdef MBU_TIMELINE
       unsigned long long te0 = clock64();
 #endif
-      mbar_wait(smem_u32(&acc_full[ab]), (p.nbuf == 2 ? (it >> 1) : it) & 1);
+      if constexpr (!BLOCK_COMMIT) mbar_wait(smem_u32(&acc_full[ab]), (p.nbuf == 2 ? (it >> 1) : it) & 1);
 #ifdef MBU_TIMELINE
       unsigned long long te1 = clock64();
 #endif
@@ -1023,6 +1027,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int64_t pix0 = TCONV ? (int64_t(tl.nb) * p.ho + yy * p.tconv_s) * p.wo + xx * p.tconv_s
                                    : (int64_t(tl.nb) * p.ho + yy) * p.wo + xx;
         const uint32_t colb = lane_base + uint32_t(ab * ACC_COLS + b * p.n_tile);
+        if constexpr (BLOCK_COMMIT) {  // single buffer: one use per tile
+          mbar_wait(smem_u32(&acc_full[b]), it & 1);
+          tc_fence_after();
+        }
         EPI_T(7 + (b >> 1));
         for (int ri = split_b ? 0 : half; ri < nr; ri += split_b ? 1 : 2) {
           // (first group, length, o0, tap dy << 16 | dx)
@@ -1452,16 +1460,16 @@ static int num_sms() {
 
 // (a separate trace-free instantiation was tried: ptxas then spills in the
 // epilogue and the N = 64 layers lose ~7%, so trace stays a runtime branch)
-template <int TAPS, bool TCONV, int LA, int CPS, bool FP4>
+template <int TAPS, bool TCONV, int LA, int CPS, bool FP4, bool BLOCK_COMMIT = false>
 static int launch_tc_impl(const tc::Params &p, const CUtensorMap &xmap, int grid, size_t smem, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    MBU_TRY(check_cuda(cudaFuncSetAttribute(tc::conv_tc_kernel<TAPS, TCONV, LA, CPS, FP4>,
+    MBU_TRY(check_cuda(cudaFuncSetAttribute(tc::conv_tc_kernel<TAPS, TCONV, LA, CPS, FP4, BLOCK_COMMIT>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
                        "cudaFuncSetAttribute"));
     configured = true;
   }
-  tc::conv_tc_kernel<TAPS, TCONV, LA, CPS, FP4><<<grid, tc::NUM_THREADS, smem, st>>>(p, xmap);
+  tc::conv_tc_kernel<TAPS, TCONV, LA, CPS, FP4, BLOCK_COMMIT><<<grid, tc::NUM_THREADS, smem, st>>>(p, xmap);
 #ifdef MBU_TIMELINE
   {
     static int call = 0;
@@ -1670,6 +1678,8 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   if (smem > 227 * 1024) return kNoFit;
   if (cv->transposed) return launch_tc_impl<1, true, tc::LA_TAP1, 4, false>(p, xmap, grid, smem, st);
   if (fp4 && cps == 4) return launch_tc_impl<9, false, tc::LA_CONV3, 4, true>(p, xmap, grid, smem, st);
+  if (fp4 && p.nbuf == 1 && p.MB <= 8 && !std::getenv("MBU_NO_BLOCK_COMMIT"))
+    return launch_tc_impl<9, false, tc::LA_CONV3, 2, true, true>(p, xmap, grid, smem, st);
   if (fp4) return launch_tc_impl<9, false, tc::LA_CONV3, 2, true>(p, xmap, grid, smem, st);
   if (cv->taps == 9) return launch_tc_impl<9, false, tc::LA_CONV3, 1, false>(p, xmap, grid, smem, st);
   return launch_tc_impl<1, false, tc::LA_TAP1, 4, false>(p, xmap, grid, smem, st);
