@@ -21,7 +21,11 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 
          "ms": 1e-3, "msecond": 1e-3, "nsecond": 1e-9}
 launches = []
 for i, m in per.items():
-    if "conv_tc_kernel<9" not in names[i] or not (", 1>" in names[i] or "true>" in names[i]):
+    nm = names[i]
+    if "conv_tc_kernel<9" not in nm:
+        continue
+    targs = [a.strip() for a in nm.split("conv_tc_kernel<", 1)[1].split(">", 1)[0].split(",")]
+    if len(targs) < 5 or targs[4] not in ("1", "true"):  # template arg FP4 (any CPS / commit variant)
         continue
     rd = m["dram__bytes_read.sum"] * scale[m["unit_dram__bytes_read.sum"]]
     wr = m["dram__bytes_write.sum"] * scale[m["unit_dram__bytes_write.sum"]]
@@ -31,7 +35,7 @@ launches.sort(key=lambda d: d["id"])
 launches = launches[:17]  # one forward: the 17 3x3 convs
 n = len(launches)
 summary = {
-    "source": src, "kernel": "conv_tc_kernel<9, false, 8, 2, true> (3x3, kind::mxf4)",
+    "source": src, "kernel": "conv_tc_kernel<9, false, 8, CPS, true, *> (3x3, kind::mxf4, every variant)",
     "launches": n,
     "dram_bytes_per_launch_avg": sum(d["dram_read"] + d["dram_write"] for d in launches) / max(n, 1),
     "dram_read_per_launch_avg": sum(d["dram_read"] for d in launches) / max(n, 1),
