@@ -1540,7 +1540,8 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   // taller tile (one buffer of up to 504 columns): each weight stage then
   // feeds up to 3 (N = 128) or 7 (N = 64) pixel blocks, cutting the weight
   // stream from L2; the un-overlapped epilogue costs a fraction of such a tile
-  p.nbuf = (fp4 && cv->kp >= 4 && cv->n_tile == 128) ? 1 : 2;
+  // (N = 64 long-K layers too: 7 blocks per tile with per-block commits, -2% on up-C3.a)
+  p.nbuf = (fp4 && cv->kp >= 4 && (cv->n_tile == 128 || cv->n_tile == 64)) ? 1 : 2;
   p.MB = fp4 ? std::min(8, (p.nbuf == 1 ? 2 * tc::FP4_COLS + 8 : tc::FP4_COLS) / cv->n_tile)
              : std::min(cv->taps == 9 ? 8 : 4, tc::ACC_COLS / cv->n_tile);  // one tap: Q <= 512
   if (x.w >= 128) {
