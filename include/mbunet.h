@@ -14,8 +14,10 @@
  *     words(pixel p, word i) = base[p * pixel_stride + word_offset + i]
  * (uint64 words, lane L of a pixel = bit L%64 of word L/64, the reference
  * layout of bitcore.py:3-18). pixel_stride == words_per_pixel for a plain
- * tensor; a larger stride lets producers write straight into their slot of
- * a concat buffer (layers.py:369-384) so concatenation costs no copy.
+ * tensor; a larger stride lets a caller address one tensor's slot inside a
+ * wider pixel. The model runner (mbu_model_*) plans a channel concat
+ * (layers.py:369-384) as a split view of its two operands' own tensors, so
+ * concatenation costs no copy and no kernel writes part of another's sector.
  *
  * Which reference interface each entry point replaces is noted beside it
  * (file:line under /root/reference/pkg/src/bitunet/). The reference is a

@@ -60,7 +60,19 @@ struct ActView {        // packed activation view, see include/mbunet.h
   int wpp;              // words per pixel of this tensor
   int stride;           // words between consecutive pixels
   int offset;           // word offset of this tensor inside each pixel slot
+  // split view (a channel concat, layers.py:369-384, planned without a copy):
+  // words [0, split) of a pixel live in `base` as above, words [split, wpp)
+  // in a second tensor `base2` with pixel stride `stride2` (offset 0).
+  // split == 0: one tensor.
+  const uint64_t *base2;
+  int stride2;
+  int split;
 };
+// address of word i of pixel pix
+__host__ __device__ __forceinline__ const uint64_t *act_word(const ActView &x, int64_t pix, int i) {
+  return (x.split && i >= x.split) ? x.base2 + pix * x.stride2 + (i - x.split)
+                                   : x.base + pix * x.stride + x.offset + i;
+}
 
 }  // namespace mbu
 

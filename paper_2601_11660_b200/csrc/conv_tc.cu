@@ -113,6 +113,10 @@ struct Params {
   const uint32_t *x32;
   int n, h, w;              // A pixel grid (conv: = output grid)
   int x_stride32, x_off32;
+  // split input (a concat planned without a copy): u32 words >= split32 of a
+  // pixel come from x2_32 (pixel stride x2_stride32, offset 0; FP4: xmap2)
+  const uint32_t *x2_32;
+  int x2_stride32, split32;  // split32 = INT_MAX: one tensor
   int halo, P, Q, R, TW, row_mode, MB;
   uint32_t p_magic;         // ceil(2^32 / P): q / P == umulhi(q, p_magic) for q < 2^16
   uint32_t nt_magic, ct_magic, rt_magic;  // same for n_tiles, col_tiles, row_tiles (t < 2^24)
@@ -465,7 +469,8 @@ __device__ __forceinline__ Run run_at(const Params &p, int jt, int g, int groups
 // the MMAs of the later blocks still run (-8% on those layers)
 template <int TAPS, bool TCONV, int LA, int CPS, bool FP4, bool BLOCK_COMMIT = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    conv_tc_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap xmap) {
+    conv_tc_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap xmap,
+                   const __grid_constant__ CUtensorMap xmap2) {
   constexpr int RAW_STAGES = LA + 1;
   constexpr int PI = prod_items(TAPS);
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -591,7 +596,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int rr = int(__umulhi(uint32_t(q), p.p_magic));
         const int iy = tl.y0 - p.halo + rr;
         const int ix = tl.x0 - p.halo + (q - rr * p.P);
-        c.off[j] = ((tl.nb * p.h + iy) * p.w + ix) * p.x_stride32 + p.x_off32;
+        c.off[j] = (tl.nb * p.h + iy) * p.w + ix;  // pixel index (the stage picks the tensor)
         if (q < p.Q && rr < strip_rows && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w) c.inb |= 1u << j;
       }
       c.t = t;
@@ -612,6 +617,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (i_t != ic.t) tile_offsets(ic, i_t);
         const int k0 = i_k * cps;
         const int cw = chunk_s[k0];  // (read once: the cp.async asm clobbers memory)
+        // a stage's chunks lie in one 128-lane block, so in one tensor of a split input
+        const bool sec = cw >= p.split32;
+        const uint32_t *xb = sec ? p.x2_32 : p.x32;
+        const int xs = sec ? p.x2_stride32 : p.x_stride32;
+        const int xo = sec ? -p.split32 : p.x_off32;
         uint32_t *dst = raw + i_slot * slot_words;
 #pragma unroll
         for (int j = 0; j < PI; ++j) {
@@ -621,12 +631,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const bool in = (ic.inb >> j) & 1;
             const uint32_t d = smem_u32(dst + q * cps);
             if constexpr (cps == 1) {
-              const uint32_t *src = p.x32 + (in ? ic.off[j] + cw : 0);
+              const uint32_t *src = in ? xb + (ic.off[j] * xs + xo + cw) : p.x32;
               asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src),
                            "r"(in ? 4 : 0)
                            : "memory");
             } else if (p.vec) {  // cps consecutive words, one copy (zero-filled out of bounds)
-              const uint32_t *src = p.x32 + (in ? ic.off[j] + cw : 0);
+              const uint32_t *src = in ? xb + (ic.off[j] * xs + xo + cw) : p.x32;
               if constexpr (cps == 4)
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src),
                              "r"(in ? 16 : 0)
@@ -642,7 +652,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             } else {
 #pragma unroll
               for (int c = 0; c < cps; ++c) {
-                const uint32_t *src = p.x32 + (in ? ic.off[j] + chunk_s[k0 + c] : 0);
+                const uint32_t *src = in ? xb + (ic.off[j] * xs + xo + chunk_s[k0 + c]) : p.x32;
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d + 4 * c), "l"(src),
                              "r"(in ? 4 : 0)
                              : "memory");
@@ -916,7 +926,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0 && (FP4 || !p.b_resident)) {
       // per stage: the weight slab (streamed) and, FP4, the raw activation box (TMA)
       int s = 0, ph = 0, g = 0, rs = 0, rph = 0;
-      if constexpr (FP4) asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
+      if constexpr (FP4) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
+        if (p.split32 != 0x7FFFFFFF) asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap2) : "memory");
+      }
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
         const Tile tl = decode_tile(p, t);
         const int8_t *src = p.b + size_t(tl.nt) * p.ks * p.b_stage_bytes;
@@ -925,11 +938,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (g >= p.rraw_stages) mbar_wait(smem_u32(&rempty[rs]), rph ^ 1);
             const uint32_t rb = smem_u32(&rfull[rs]);
             mbar_arrive_expect_tx(rb, p.rraw_box_bytes);
+            // the stage's 128-lane block: u32 word blk of the (logical) pixel
+            const int blk = 4 * (chunk_s[2 * (FP4 ? CPS / 2 : 1) * k] >> 2);
+            const bool sec = blk >= p.split32;
             asm volatile(
                 "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
                 "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(smem + p.off_rraw + rs * p.rraw_bytes)),
-                "l"(&xmap), "r"(p.x_off32 + 4 * (chunk_s[2 * (FP4 ? CPS / 2 : 1) * k] >> 2)), "r"(tl.x0 - p.halo), "r"(tl.y0 - p.halo),
-                "r"(tl.nb), "r"(rb)
+                "l"(sec ? &xmap2 : &xmap), "r"(sec ? blk - p.split32 : p.x_off32 + blk), "r"(tl.x0 - p.halo),
+                "r"(tl.y0 - p.halo), "r"(tl.nb), "r"(rb)
                 : "memory");
             if (++rs == p.rraw_stages) {
               rs = 0;
@@ -1461,7 +1477,8 @@ static int num_sms() {
 // (a separate trace-free instantiation was tried: ptxas then spills in the
 // epilogue and the N = 64 layers lose ~7%, so trace stays a runtime branch)
 template <int TAPS, bool TCONV, int LA, int CPS, bool FP4, bool BLOCK_COMMIT = false>
-static int launch_tc_impl(const tc::Params &p, const CUtensorMap &xmap, int grid, size_t smem, cudaStream_t st) {
+static int launch_tc_impl(const tc::Params &p, const CUtensorMap &xmap, const CUtensorMap &xmap2, int grid,
+                          size_t smem, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
     MBU_TRY(check_cuda(cudaFuncSetAttribute(tc::conv_tc_kernel<TAPS, TCONV, LA, CPS, FP4, BLOCK_COMMIT>,
@@ -1469,7 +1486,7 @@ static int launch_tc_impl(const tc::Params &p, const CUtensorMap &xmap, int grid
                        "cudaFuncSetAttribute"));
     configured = true;
   }
-  tc::conv_tc_kernel<TAPS, TCONV, LA, CPS, FP4, BLOCK_COMMIT><<<grid, tc::NUM_THREADS, smem, st>>>(p, xmap);
+  tc::conv_tc_kernel<TAPS, TCONV, LA, CPS, FP4, BLOCK_COMMIT><<<grid, tc::NUM_THREADS, smem, st>>>(p, xmap, xmap2);
 #ifdef MBU_TIMELINE
   {
     static int call = 0;
@@ -1530,8 +1547,12 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   p.w = x.w;
   p.x_stride32 = x.stride * 2;
   p.x_off32 = x.offset * 2;
+  p.x2_32 = reinterpret_cast<const uint32_t *>(x.split ? x.base2 : x.base);
+  p.x2_stride32 = x.split ? x.stride2 * 2 : 0;
+  p.split32 = x.split ? x.split * 2 : 0x7FFFFFFF;
   // producers index the input with 32-bit word offsets
-  if ((int64_t(x.n) * x.h * x.w + 2 * int64_t(x.w) + 4) * p.x_stride32 >= (int64_t(1) << 31))
+  if ((int64_t(x.n) * x.h * x.w + 2 * int64_t(x.w) + 4) * std::max(p.x_stride32, p.x2_stride32) >=
+      (int64_t(1) << 31))
     return fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv input larger than 2^31 words");
   p.halo = cv->taps == 9 ? 1 : 0;
   p.n_tile = cv->n_tile;
@@ -1579,7 +1600,10 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   if (kcs % cps) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 one-tap conv needs whole 128-lane blocks");
   p.ks = kcs / cps;
   p.vec = fp4 ? (cv->pair_consec && p.x_stride32 % 2 == 0 && p.x_off32 % 2 == 0)
-              : ((cv->chunk_consec >> (cps >> 1)) & 1) && p.x_stride32 % cps == 0 && p.x_off32 % cps == 0;
+              : ((cv->chunk_consec >> (cps >> 1)) & 1) && p.x_stride32 % cps == 0 && p.x_off32 % cps == 0 &&
+                    (!x.split || (p.x2_stride32 % cps == 0 && p.split32 % cps == 0));
+  if (x.split && (x.split % 2 || x.split > x.wpp))
+    return fail(MBU_ERR_LAYOUT, "split input view must break at a 128-lane block");
   p.a_chunk_bytes = uint32_t(Q) * 32;
   p.a_stage_bytes = uint32_t((size_t(Q) * 32 * (fp4 ? cps / 2 : cps) + 1023) / 1024 * 1024);
   p.b_stage_bytes = uint32_t(cv->b_stage_bytes * (fp4 ? cps / 2 : cps));
@@ -1587,8 +1611,9 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   const int raw_stages = (cv->taps == 9 ? tc::LA_CONV3 : tc::LA_TAP1) + 1;
   // shared memory: [header][A stages][B stages | resident B][raw ring][runs, biases][ones][slabs][slab map]
   // (FP4: the raw ring holds TMA boxes of one 128-lane block per strip pixel)
-  CUtensorMap xmap;
+  CUtensorMap xmap, xmap2;
   std::memset(&xmap, 0, sizeof(xmap));
+  std::memset(&xmap2, 0, sizeof(xmap2));
   p.raw_rows = p.R + 2 * p.halo;
   if (fp4) {
     p.rraw_box_bytes = uint32_t(16) * p.P * p.raw_rows;
@@ -1601,6 +1626,14 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
     if (p.P > 256 || p.raw_rows > 256 || p.x_stride32 % 4 || p.x_off32 % 4 ||
         (reinterpret_cast<uintptr_t>(x.base) & 15) || !make_tmap_u32_4d(&xmap, x.base, dims, strides, box))
       return fail(MBU_ERR_UNSUPPORTED, "tcgen05 FP4 conv: raw activation tensor map unavailable");
+    if (x.split) {  // the concat's second operand: its own contiguous tensor
+      const uint64_t d2[4] = {uint64_t(p.x2_stride32), uint64_t(x.w), uint64_t(x.h), uint64_t(x.n)};
+      const uint64_t s2[3] = {uint64_t(p.x2_stride32) * 4, uint64_t(p.x2_stride32) * 4 * x.w,
+                              uint64_t(p.x2_stride32) * 4 * x.w * x.h};
+      if (p.x2_stride32 % 4 || (reinterpret_cast<uintptr_t>(x.base2) & 15) ||
+          !make_tmap_u32_4d(&xmap2, x.base2, d2, s2, box))
+        return fail(MBU_ERR_UNSUPPORTED, "tcgen05 FP4 conv: second raw activation tensor map unavailable");
+    }
   }
   const size_t raw_bytes = fp4 ? size_t(p.rraw_stages) * p.rraw_bytes : size_t(raw_stages) * Q * cps * 4;
   const size_t runs_bytes = size_t(cv->n_tiles) * 9 * 16 + size_t(cv->n_tiles) * cv->n_tile * 4;
@@ -1677,13 +1710,13 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   const int grid = int(std::min<int64_t>(tiles, num_sms()));
   const size_t smem = std::max<size_t>(smem_total, tc::MIN_SMEM);
   if (smem > 227 * 1024) return kNoFit;
-  if (cv->transposed) return launch_tc_impl<1, true, tc::LA_TAP1, 4, false>(p, xmap, grid, smem, st);
-  if (fp4 && cps == 4) return launch_tc_impl<9, false, tc::LA_CONV3, 4, true>(p, xmap, grid, smem, st);
+  if (cv->transposed) return launch_tc_impl<1, true, tc::LA_TAP1, 4, false>(p, xmap, xmap2, grid, smem, st);
+  if (fp4 && cps == 4) return launch_tc_impl<9, false, tc::LA_CONV3, 4, true>(p, xmap, xmap2, grid, smem, st);
   if (fp4 && p.nbuf == 1 && p.MB <= 8 && !std::getenv("MBU_NO_BLOCK_COMMIT"))
-    return launch_tc_impl<9, false, tc::LA_CONV3, 2, true, true>(p, xmap, grid, smem, st);
-  if (fp4) return launch_tc_impl<9, false, tc::LA_CONV3, 2, true>(p, xmap, grid, smem, st);
-  if (cv->taps == 9) return launch_tc_impl<9, false, tc::LA_CONV3, 1, false>(p, xmap, grid, smem, st);
-  return launch_tc_impl<1, false, tc::LA_TAP1, 4, false>(p, xmap, grid, smem, st);
+    return launch_tc_impl<9, false, tc::LA_CONV3, 2, true, true>(p, xmap, xmap2, grid, smem, st);
+  if (fp4) return launch_tc_impl<9, false, tc::LA_CONV3, 2, true>(p, xmap, xmap2, grid, smem, st);
+  if (cv->taps == 9) return launch_tc_impl<9, false, tc::LA_CONV3, 1, false>(p, xmap, xmap2, grid, smem, st);
+  return launch_tc_impl<1, false, tc::LA_TAP1, 4, false>(p, xmap, xmap2, grid, smem, st);
 }
 
 }  // namespace mbu

@@ -64,12 +64,11 @@ __global__ void __launch_bounds__(256) conv_popcount_kernel(
     int dpos = 0, dneg = 0, corr = 0;
     auto visit = [&](int tap, int iy, int ix) {
       const bool inb = iy >= 0 && iy < x.h && ix >= 0 && ix < x.w;
-      const uint64_t *xp =
-          x.base + (int64_t(nb * x.h + (inb ? iy : 0)) * x.w + (inb ? ix : 0)) * x.stride + x.offset;
+      const int64_t px = int64_t(nb * x.h + (inb ? iy : 0)) * x.w + (inb ? ix : 0);
       const uint64_t *wp = pos + (int64_t(o) * taps + tap) * wpp;
       const uint64_t *wn = MASKED ? neg + (int64_t(o) * taps + tap) * wpp : nullptr;
       for (int i = 0; i < wpp; ++i) {
-        const uint64_t a = inb ? __ldg(xp + i) : 0ull;
+        const uint64_t a = inb ? __ldg(act_word(x, px, i)) : 0ull;
         dpos += __popcll(a ^ __ldg(wp + i));
         if (MASKED) dneg += __popcll(a ^ __ldg(wn + i));
       }
@@ -164,6 +163,7 @@ __global__ void __launch_bounds__(256) maxpool2_kernel(ActView x, uint64_t *__re
 
 int launch_maxpool(const ActView &x, uint64_t *out, int out_stride, int out_offset,
                    cudaStream_t st) {
+  if (x.split) return fail(MBU_ERR_UNSUPPORTED, "maxpool2 of a split (concat) view");
   const int64_t total = int64_t(x.n) * (x.h / 2) * (x.w / 2) * (x.wpp / 2);
   if (total == 0) return MBU_OK;
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 64);
@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(256) fconv_plain_kernel(
 int launch_fconv(const mbu_fconv *fc, const double *x_f64, const ActView &xb, int n, int h,
                  int w, double *acc, uint64_t *bits, int out_stride, int out_offset,
                  uint8_t *mask, cudaStream_t st) {
+  if (!x_f64 && xb.split) return fail(MBU_ERR_UNSUPPORTED, "float conv of a split (concat) view");
   const int ho = (h + 2 * fc->pad - fc->kh) / fc->stride + 1;
   const int wo = (w + 2 * fc->pad - fc->kw) / fc->stride + 1;
   const int64_t pix = int64_t(n) * ho * wo;

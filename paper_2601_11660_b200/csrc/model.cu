@@ -3,9 +3,13 @@
 //
 // Planning resolves every layer's output to a view (buffer, pixel stride,
 // word offset) inside one caller-provided workspace. Concatenation
-// (layers.py:369-384) is resolved at plan time: both operands' producers
-// write directly into their word ranges of the concat buffer, so a concat
-// step launches nothing and the skip tensor is never copied. The forward
+// (layers.py:369-384) is resolved at plan time into a split view: both
+// operands keep their own contiguous tensors and the consuming conv reads
+// words [0, wpp_a) of a pixel from the first and the rest from the second
+// (conv_tc: one TMA tensor map per operand). A concat step launches nothing,
+// the skip tensor is never copied, and no kernel writes part of a 32-B
+// sector that another kernel fills (the half-sector read-modify-write an
+// interleaved concat buffer costs at DRAM). The forward
 // then enqueues one kernel per conv / pool step on the caller's stream, which
 // the Python host captures into a CUDA graph.
 #include <cuda_runtime.h>
@@ -30,8 +34,7 @@ struct Layer {
   int n = 0, h = 0, w = 0;
   int out_kind = 0;      // 0 packed bits, 1 float64 (logits)
   int wpp = 0;           // bits: words per pixel; float: channels
-  int buf = -1, stride = 0, offset = 0;
-  int claimed_by = -1;   // concat that owns this layer's storage
+  int buf = -1, stride = 0, offset = 0;  // (concat: no buffer, a split view of src + skip)
   int acc_buf = -1, acc_c = 0, acc_f64 = 0;
 };
 
@@ -129,7 +132,6 @@ int mbu_model_plan(mbu_model *m, int n, int H, int W, int trace, size_t *ws_byte
   for (int i = 0; i < int(L.size()); ++i) {
     Layer &l = L[i];
     l.src = i - 1;
-    l.claimed_by = -1;
     l.buf = -1;
     l.acc_buf = -1;
     if (l.type == MBU_LAYER_FLOAT_CONV) {
@@ -177,32 +179,26 @@ int mbu_model_plan(mbu_model *m, int n, int H, int W, int trace, size_t *ws_byte
     }
     cn = l.n; ch = l.h; cw = l.w; ckind = l.out_kind; cwpp = l.wpp;
   }
-  // ---- concat claims
+  // ---- concat operands: plain tensors; only bit convs read a concat
   for (int i = 0; i < int(L.size()); ++i) {
     if (L[i].type != MBU_LAYER_CONCAT) continue;
-    for (int opnd : {L[i].src, L[i].skip}) {
-      if (opnd < 0 || L[opnd].type == MBU_LAYER_CONCAT || L[opnd].claimed_by >= 0)
-        return fail(MBU_ERR_UNSUPPORTED, "concat operand layout cannot be aliased");
-      L[opnd].claimed_by = i;
-    }
+    for (int opnd : {L[i].src, L[i].skip})
+      if (opnd < 0 || L[opnd].type == MBU_LAYER_CONCAT)
+        return fail(MBU_ERR_UNSUPPORTED, "concat of a concat is not supported");
+    for (int j = i + 1; j < int(L.size()); ++j)
+      if ((L[j].src == i || (L[j].type == MBU_LAYER_CONCAT && L[j].skip == i)) &&
+          L[j].type != MBU_LAYER_BIT_CONV && L[j].type != MBU_LAYER_BIT_TCONV)
+        return fail(MBU_ERR_UNSUPPORTED, "a concat must feed a bit conv");
   }
   // ---- buffers
   for (int i = 0; i < int(L.size()); ++i) {
     Layer &l = L[i];
-    if (l.out_kind == 0 && l.claimed_by < 0) {
+    if (l.out_kind == 0 && l.type != MBU_LAYER_CONCAT) {
       l.buf = add_buf(m, size_t(l.n) * l.h * l.w * l.wpp * 8);
       l.stride = l.wpp;
       l.offset = 0;
     }
     if (l.acc_c) l.acc_buf = add_buf(m, size_t(l.n) * l.h * l.w * l.acc_c * (l.acc_f64 ? 8 : 4));
-  }
-  for (int i = 0; i < int(L.size()); ++i) {
-    Layer &l = L[i];
-    if (l.claimed_by < 0) continue;
-    const Layer &c = L[l.claimed_by];
-    l.buf = c.buf;
-    l.stride = c.stride;
-    l.offset = (i == c.src) ? 0 : L[c.src].wpp;
   }
   m->planned = 1;
   *ws_bytes = m->ws;
@@ -218,14 +214,20 @@ int mbu_forward(mbu_model *m, const double *image, double *logits, uint8_t *mask
   char *base = static_cast<char *>(ws);
   auto view_of = [&](int i) -> ActView {
     const Layer &l = m->layers[i];
+    if (l.type == MBU_LAYER_CONCAT) {  // split view: src words, then the skip's
+      const Layer &a = m->layers[l.src], &b = m->layers[l.skip];
+      return ActView{reinterpret_cast<const uint64_t *>(base + m->buf_off[a.buf]), l.n, l.h, l.w, l.wpp,
+                     a.stride, a.offset, reinterpret_cast<const uint64_t *>(base + m->buf_off[b.buf]),
+                     b.stride, a.wpp};
+    }
     return ActView{reinterpret_cast<const uint64_t *>(base + m->buf_off[l.buf]), l.n, l.h, l.w,
-                   l.wpp, l.stride, l.offset};
+                   l.wpp, l.stride, l.offset, nullptr, 0, 0};
   };
   const bool timed = m->timing && int(m->events.size()) == int(m->layers.size()) + 1;
   for (int i = 0; i < int(m->layers.size()); ++i) {
     const Layer &l = m->layers[i];
     if (timed) MBU_TRY(check_cuda(cudaEventRecord(m->events[i], st), "cudaEventRecord"));
-    uint64_t *out = l.out_kind == 0 ? reinterpret_cast<uint64_t *>(base + m->buf_off[l.buf]) : nullptr;
+    uint64_t *out = l.buf >= 0 ? reinterpret_cast<uint64_t *>(base + m->buf_off[l.buf]) : nullptr;
     void *acc = l.acc_buf >= 0 ? base + m->buf_off[l.acc_buf] : nullptr;
     int in_h = l.src < 0 ? m->H : m->layers[l.src].h;
     int in_w = l.src < 0 ? m->W : m->layers[l.src].w;

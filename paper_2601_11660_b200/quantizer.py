@@ -234,3 +234,13 @@ def live_bundle(config, rng: np.random.Generator) -> WeightBundle:
             be.var = (rng.uniform(0.5, 2.0, c) * k_eff).astype(np.float32)
             be.beta = rng.normal(0.0, 0.3, c).astype(np.float32)
     return bundle
+
+
+def bench_frame(index: int, height: int, width: int) -> np.ndarray:
+    """Synthetic frame ``index`` of the benchmark stream: float64 (H, W, 3) in [0, 1).
+
+    ``bench.py`` fills its batches with these and the big-shape golden
+    fixtures (``tests/golden/make_golden_big.py``) are the reference's forward
+    of the same frames, so the benchmarked inputs are parity-pinned.
+    """
+    return np.random.default_rng(1000 + index).random((height, width, 3))

@@ -48,6 +48,7 @@ class DeviceModel:
         self.names, self.kinds = [], []
         self.out_segments = []  # per layer: output lane layout (bit layers)
         self.out_channels = []  # per layer: logical channel count
+        self.concat_skip = {}  # concat layer -> its skip operand (the other one is the layer before)
         h = ctypes.c_void_p()
         _lib.call("mbu_model_create", ctypes.byref(h), self.device.index)
         self.handle = h
@@ -80,6 +81,7 @@ class DeviceModel:
                 elif kind == "concat":
                     j = index[layer.concat_with]
                     _lib.call("mbu_model_add_concat", h, j)
+                    self.concat_skip[i] = j
                     shift = segment_lanes(segs)
                     segs = segs + tuple(ChannelSegment(s.lane_offset + shift, s.count)
                                         for s in self.out_segments[j])
@@ -109,6 +111,9 @@ class DeviceModel:
     def run(self, image, logits, mask, workspace, path=_lib.PATH_AUTO, stream=None):
         """Enqueue one forward on ``stream`` (all arguments CUDA tensors)."""
         s = _stream(self.device) if stream is None else ctypes.c_void_p(stream.cuda_stream)
+        # the native plan is per model handle: run only what it was planned for
+        if self.planned is None or tuple(image.shape[:3]) != self.planned[:3]:
+            raise EngineError(f"image {tuple(image.shape)} does not match the plan {self.planned}")
         _lib.call("mbu_forward", self.handle, _ptr(image), _ptr(logits), _ptr(mask),
                   _ptr(workspace), workspace.numel() * workspace.element_size(), path, s)
 
@@ -134,13 +139,18 @@ class DeviceModel:
                     out_off=None if ob.value == nofs else ob.value,
                     acc_off=None if ab.value == nofs else ab.value, acc_c=accc.value)
 
-    def read_trace(self, workspace: torch.Tensor, logits_np: np.ndarray) -> dict:
-        """Assemble the reference trace dict from the planned workspace."""
+    def read_trace(self, workspace: torch.Tensor, logits_np: np.ndarray, frames=None) -> dict:
+        """Assemble the reference trace dict from the planned workspace.
+
+        ``frames`` (a slice of the batch axis) restricts the copy to those
+        frames, sliced on the device: a full-size batch-8 trace is ~35 GB."""
         ws = workspace.view(torch.uint8)
+        sel = slice(None) if frames is None else frames
         trace = {}
         for i, name in enumerate(self.names):
             info = self.layer_info(i)
             n, h, w = info["n"], info["h"], info["w"]
+            n_sel = len(range(n)[sel])
             acc = None
             if info["acc_off"] is not None:
                 c = info["acc_c"]
@@ -148,16 +158,24 @@ class DeviceModel:
                 nbytes = n * h * w * c * (8 if is_f else 4)
                 raw = ws[info["acc_off"]:info["acc_off"] + nbytes]
                 acc = raw.view(torch.float64 if is_f else torch.int32).reshape(n, h, w, c)
-                acc = acc.cpu().numpy()
+                acc = acc[sel].cpu().numpy()
             if info["kind"] == 1:  # the head: float logits
                 out = logits_np
                 acc = logits_np
+            elif i in self.concat_skip:
+                # planned as a split view (no concat buffer): the reference's
+                # concat words are operand a's words, then operand b's
+                # (layers.py:369-384; wpp_a is whole 128-lane blocks)
+                a, b = trace[self.names[i - 1]]["out"], trace[self.names[self.concat_skip[i]]]["out"]
+                out = BitTensor(n_sel, h, w, self.out_channels[i],
+                                np.ascontiguousarray(np.concatenate([a.words, b.words], axis=-1)),
+                                self.out_segments[i])
             else:
                 stride, off, wpp = info["stride"], info["offset"], info["wpp"]
                 nbytes = n * h * w * stride * 8
                 raw = ws[info["out_off"]:info["out_off"] + nbytes].view(torch.int64)
-                words = raw.reshape(n, h, w, stride)[..., off:off + wpp].cpu().numpy()
-                out = BitTensor(n, h, w, self.out_channels[i],
+                words = raw.reshape(n, h, w, stride)[sel, ..., off:off + wpp].cpu().numpy()
+                out = BitTensor(n_sel, h, w, self.out_channels[i],
                                 np.ascontiguousarray(words).view(np.uint64),
                                 self.out_segments[i])
             trace[name] = {"acc": acc, "out": out}
@@ -239,7 +257,10 @@ class Engine:
     def __init__(self, model, batch: int, device=None, use_graph: bool = True,
                  path=_lib.PATH_AUTO, with_logits: bool = True):
         cfg = model.config
-        self.dm = _device_model(model, device)
+        # an Engine owns its model handle: the native plan (batch, buffer
+        # offsets) is per handle, so a forward() or another Engine on the same
+        # model can never re-plan the buffers this Engine's graphs replay
+        self.dm = DeviceModel(model, cuda_device(device))
         self.device = self.dm.device
         self.batch = batch
         self.shape = (batch, cfg.height, cfg.width, cfg.in_channels)
