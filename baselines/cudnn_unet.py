@@ -51,13 +51,22 @@ class FP16UNet(nn.Module):
 
 
 class CudnnUNetRunner:
-    """Batch-fixed FP16 U-Net forward replayed from a CUDA graph."""
+    """Batch-fixed FP16 U-Net forward replayed from a CUDA graph.
 
-    def __init__(self, cfg, batch: int, device):
+    ``fused=True`` is the stronger baseline: the same network through
+    ``torch.compile`` (Inductor keeps cuDNN for the convolutions and fuses the
+    bias / ReLU / concat traffic around them into generated kernels), then
+    captured in the same CUDA graph. Only the baseline is compiled; the MBU-Net
+    path never is.
+    """
+
+    def __init__(self, cfg, batch: int, device, fused: bool = False):
         torch.backends.cudnn.benchmark = True
         torch.backends.cudnn.allow_tf32 = True
         self.device = device
         self.net = FP16UNet(cfg).to(device).half().to(memory_format=torch.channels_last).eval()
+        if fused:
+            self.net = torch.compile(self.net, dynamic=False)
         self.x = torch.randn(batch, cfg.in_channels, cfg.height, cfg.width, device=device,
                              dtype=torch.float16).to(memory_format=torch.channels_last)
         self.stream = torch.cuda.Stream(device)

@@ -164,6 +164,10 @@ int mbu_decode_raster(const void *raster, int64_t count, int bytes_per_sample, i
  * quantizer.py:86-102; delta = t * mean|w| computed by the caller). */
 int mbu_quantize_weights(const float *w, int64_t n, int binary, double delta, int8_t *out,
                          void *stream);
+/* Same for float64 weights. Both compare in float64, as numpy does for a
+ * float32 / float64 array against the float64 delta. */
+int mbu_quantize_weights_f64(const double *w, int64_t n, int binary, double delta, int8_t *out,
+                             void *stream);
 /* fuse_bn_sign (layers.py:455-505): per-channel int32 thresholds and codes
  * (DIR_GE 0, DIR_LE 1, CONST_NEG 2, CONST_POS 3) of the float64 predicate
  * gamma*((acc + bias) - mean)/sqrt(var + eps) + beta >= 0. Device pointers;

@@ -37,6 +37,7 @@ _SIGS = {
     "mbu_argmax": (_i, [_vp, _i64, _i, _vp, _vp]),
     "mbu_decode_raster": (_i, [_vp, _i64, _i, _i, _vp, _vp]),
     "mbu_quantize_weights": (_i, [_vp, _i64, _i, _c.c_double, _vp, _vp]),
+    "mbu_quantize_weights_f64": (_i, [_vp, _i64, _i, _c.c_double, _vp, _vp]),
     "mbu_fuse_bn_sign": (_i, [_vp, _vp, _vp, _vp, _c.c_double, _vp, _i, _vp, _vp, _vp]),
     "mbu_conv_create": (_i, [_c.POINTER(_vp), _i, _i, _i, _i, _i, _i, _i, _i, _i, _i,
                              _vp, _vp, _vp, _vp, _vp, _vp]),

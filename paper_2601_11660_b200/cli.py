@@ -155,32 +155,37 @@ def _build_parser() -> argparse.ArgumentParser:
     return parser
 
 
+# Exit-code contract of the reference CLI (pkg/src/bitunet/cli.py:474-503), as a
+# table: the first row whose classes match the raised exception wins.
+_EXIT_TABLE = (
+    ((FormatError, OSError), _FORMAT_EXIT, "error"),
+    ((UnsupportedConfigError, ValueAlphabetError, PlaneOverlapError), _CONFIG_EXIT, "error"),
+    ((ShapeError, LayoutError), _SHAPE_EXIT, "error"),
+    ((EngineError,), _INTERNAL_EXIT, "error"),
+    ((Exception,), _INTERNAL_EXIT, "internal error"),
+)
+
+
+def _exit_code(exc: BaseException) -> int:
+    for classes, code, label in _EXIT_TABLE:
+        if isinstance(exc, classes):
+            detail = str(exc) if label == "error" else f"{type(exc).__name__}: {exc}"
+            print(f"{label}: {detail}", file=sys.stderr)
+            return code
+    raise exc
+
+
 def main(argv=None) -> int:
+    """CLI entry; returns the process exit code (usage errors: argparse's 2)."""
     parser = _build_parser()
     try:
         args = parser.parse_args(argv)
-    except SystemExit as exc:  # argparse exits 2 on usage errors, 0 on --help
-        return int(exc.code or 0)
+    except SystemExit as stop:
+        return int(stop.code or 0)
     try:
         return args.handler(args)
-    except FormatError as exc:
-        print(f"error: {exc}", file=sys.stderr)
-        return _FORMAT_EXIT
-    except (UnsupportedConfigError, ValueAlphabetError, PlaneOverlapError) as exc:
-        print(f"error: {exc}", file=sys.stderr)
-        return _CONFIG_EXIT
-    except (ShapeError, LayoutError) as exc:
-        print(f"error: {exc}", file=sys.stderr)
-        return _SHAPE_EXIT
-    except OSError as exc:
-        print(f"error: {exc}", file=sys.stderr)
-        return _FORMAT_EXIT
-    except EngineError as exc:
-        print(f"error: {exc}", file=sys.stderr)
-        return _INTERNAL_EXIT
-    except Exception as exc:  # noqa: BLE001 - the CLI boundary reports everything
-        print(f"internal error: {type(exc).__name__}: {exc}", file=sys.stderr)
-        return _INTERNAL_EXIT
+    except Exception as exc:  # noqa: BLE001 - mapped through _EXIT_TABLE
+        return _exit_code(exc)
 
 
 if __name__ == "__main__":

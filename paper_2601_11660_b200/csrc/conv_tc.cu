@@ -148,7 +148,8 @@ struct Params {
   // FP4: raw activation blocks arrive by TMA (one box of 16 B x P x strip rows per stage)
   uint32_t off_rraw, rraw_bytes, rraw_box_bytes;
   int rraw_stages, raw_rows;
-  int nbuf;                 // accumulator buffers: 2 (epilogue overlaps the next tile) or 1 (long K, big M)
+  int nbuf;                 // accumulator buffers: 2-3 (epilogue overlaps the next tiles) or 1 (long K, big M)
+  int buf_cols;             // TMEM columns between accumulator buffers
   int n_slabs;
   const int8_t *bias_slab;  // [n_slabs][khalf][n_tile][16]: s8, sum(lo) + 127*sum(hi) = bias
   const int32_t *slab_of_nt;
@@ -298,6 +299,26 @@ __device__ __forceinline__ void umma9_fp4(uint32_t tmem_d, uint64_t a_c, uint64_
       "add.s64 b, b, %4;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %5, [%6], [%6], p;\n\t}" ::"r"(tmem_d),
       "l"(a_c), "l"(b0), "l"(pp), "l"(bs), "r"(idesc), "r"(sf)
+      : "memory");
+}
+// one kind::mxf4 MMA from 32-bit descriptor halves. The caller keeps every
+// address computation in 32-bit, warp-uniform arithmetic (the high words are
+// constant and an offset never carries out of the 14-bit start field), so
+// ptxas issues the MMA straight from uniform registers: a few UIADD3/UMOV per
+// MMA instead of ~14 instructions of 64-bit vector adds, R2UR.BROADCAST and
+// VOTEU. That matters because the MMA warp shares its SM sub-partition with
+// ALU-bound epilogue warps: measured (tools/ubench_fp4, mxf4_strip_alu_noise)
+// a 14-instruction issue path slows N = 64 MMAs from 48 to ~70 cycles.
+__device__ __forceinline__ void mma_fp4(uint32_t d, uint32_t alo, uint32_t ahi, uint32_t blo, uint32_t bhi,
+                                        uint32_t idesc, uint32_t sfa, uint32_t sfb, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 a, b;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %8, 0;\n\t"
+      "mov.b64 a, {%1, %2};\n\t"
+      "mov.b64 b, {%3, %4};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %5, [%6], [%7], p;\n\t}" ::"r"(d),
+      "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(sfa), "r"(sfb), "r"(acc)
       : "memory");
 }
 // one kind::mxf4 MMA (bias MMAs): acc = 0 overwrites, separate A / B scale columns
@@ -478,7 +499,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t *empty = full + MAX_STAGES;
   uint64_t *acc_full = empty + MAX_STAGES;
   uint64_t *acc_empty = acc_full + 8;  // (acc_full[8]: per-block barriers under BLOCK_COMMIT)
-  uint64_t *bres = acc_empty + 2;  // resident weights landed
+  uint64_t *bres = acc_empty + 4;  // resident weights landed
   uint64_t *rfull = bres + 1;       // [8] FP4: raw box landed (TMA)
   uint64_t *rempty = rfull + 8;     // [8] FP4: raw box consumed (producers)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rempty + 8);
@@ -486,7 +507,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t *a_base = smem + SMEM_HEADER;
   uint8_t *b_base = smem + p.off_b;
 
-  const int warp = threadIdx.x >> 5;
+  // warp index through a shuffle: ptxas then knows it is warp-uniform, so the
+  // role branches below are uniform and the MMA warp's descriptor arithmetic
+  // stays on the uniform datapath (no BRA.DIV / R2UR.BROADCAST per MMA)
+  const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const int S = p.stages;
 
@@ -501,7 +525,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(smem_u32(&rempty[i]), PROD_THREADS);
     }
     for (int i = 0; i < 8; ++i) mbar_init(smem_u32(&acc_full[i]), 1);
-    for (int i = 0; i < 2; ++i) mbar_init(smem_u32(&acc_empty[i]), EPI_THREADS);
+    for (int i = 0; i < 3; ++i) mbar_init(smem_u32(&acc_empty[i]), EPI_THREADS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = threadIdx.x; i < p.kc; i += blockDim.x) chunk_s[i] = p.chunk_word[i];
@@ -830,9 +854,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint64_t slab_desc0 = umma_desc(smem_u32(smem + p.off_slab), b_lbo, sbo);
       const int32_t *smap = reinterpret_cast<const int32_t *>(smem + p.off_slabmap);
       if (p.b_resident) mbar_wait(smem_u32(bres), 0);
-      int s = 0, ph = 0, it = 0;
+      int s = 0, ph = 0, it = 0, ab = 0, aph = 0;  // accumulator buffer ring: index, phase
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-        const int ab = p.nbuf == 2 ? (it & 1) : 0;
         const int nt = t - fdiv(t, p.nt_magic) * p.n_tiles;
         // (read before the wait: a shared load issued behind the tensor core's
         // operand reads takes hundreds of cycles, keep it off the issue path)
@@ -840,16 +863,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #ifdef MBU_TIMELINE
         unsigned long long tl0 = clock64();
 #endif
-        mbar_wait(smem_u32(&acc_empty[ab]), (p.nbuf == 2 ? (it >> 1) : it) & 1);
+        mbar_wait(smem_u32(&acc_empty[ab]), aph);
 #ifdef MBU_TIMELINE
         unsigned long long tl1 = clock64();
 #endif
         tc_fence_after();
-        const uint32_t d0 = tmem + uint32_t(ab * ACC_COLS);
+        const uint32_t d0 = tmem + uint32_t(ab * p.buf_cols);
         if (FP4 && p.mma_bias) {  // bias = lo (K 0-31, A scale 1) + 256 * hi (K 32-63, A scale 2^8)
-          const uint64_t sd = slab_desc0 + uint64_t(slab) * uint64_t(p.n_tile * 2);
+          const uint32_t sd = uint32_t(slab_desc0) + uint32_t(slab * p.n_tile * 2);
           for (int b = 0; b < p.MB; ++b)
-            umma1_fp4(d0 + uint32_t(b * p.n_tile), ones_desc, sd, p.idesc, tmem + p.sf256, tmem + p.sf1, 0u);
+            mma_fp4(d0 + uint32_t(b * p.n_tile), uint32_t(ones_desc), uint32_t(ones_desc >> 32), sd,
+                    uint32_t(slab_desc0 >> 32), p.idesc, tmem + p.sf256, tmem + p.sf1, 0u);
         } else if (p.mma_bias) {
           const uint64_t sd = slab_desc0 + uint64_t(slab) * uint64_t(p.n_tile * 2);
           for (int b = 0; b < p.MB; ++b) umma1_i8_first(d0 + uint32_t(b * p.n_tile), ones_desc, sd, p.idesc);
@@ -874,12 +898,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #else
           if constexpr (FP4) {
 #endif
+            // 32-bit uniform descriptor arithmetic (see mma_fp4)
+            const uint32_t a_hi = uint32_t(a_desc0 >> 32), b_hi = uint32_t(b_desc0 >> 32);
+            const uint32_t a_lo = uint32_t(a_s), b_lo = uint32_t(b_s), P32 = uint32_t(p.P);
+            const uint32_t bs32 = uint32_t(bs), sf = tmem + p.sf1;
             for (int b = 0; b < p.MB; ++b) {
-              umma9_fp4(d0 + uint32_t(b * p.n_tile), a_s + uint64_t(block_q0(p, b)), b_s, pp, bs, p.idesc,
-                        tmem + p.sf1);
-              if constexpr (CPS == 4)
-                umma9_fp4(d0 + uint32_t(b * p.n_tile), a_s + uint64_t(p.a_chunk_bytes >> 4) + uint64_t(block_q0(p, b)),
-                          b_s + uint64_t(p.b_pair_bytes >> 4), pp, bs, p.idesc, tmem + p.sf1);
+              const uint32_t d = d0 + uint32_t(b * p.n_tile);
+#pragma unroll
+              for (int pr = 0; pr < CPS / 2; ++pr) {  // chunk pairs of this stage
+                const uint32_t ac = a_lo + uint32_t(block_q0(p, b)) + uint32_t(pr * (p.a_chunk_bytes >> 4));
+                const uint32_t bc = b_lo + uint32_t(pr * (p.b_pair_bytes >> 4));
+#pragma unroll
+                for (int tap = 0; tap < 9; ++tap)
+                  mma_fp4(d, ac + uint32_t(tap / 3 - 1) * P32 + uint32_t(tap % 3 - 1), a_hi, bc + uint32_t(tap) * bs32,
+                          b_hi, p.idesc, sf, sf, 1u);
+              }
               if constexpr (BLOCK_COMMIT) {
                 if (k == p.ks - 1) umma_commit_elect(smem_u32(&acc_full[b]));
               }
@@ -903,6 +936,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         if constexpr (!BLOCK_COMMIT) umma_commit_elect(smem_u32(&acc_full[ab]));
+        if (++ab == p.nbuf) {
+          ab = 0;
+          aph ^= 1;
+        }
         MMA_T(12);
 #ifdef MBU_TIMELINE
         if (blockIdx.x == 0 && lane == 0 && it < 64) {
@@ -999,7 +1036,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(float(int(v[i])) + 0.5f);
               }
-              tmem_st32(lane_base + uint32_t(ab * ACC_COLS + b * p.n_tile + gg * 32), v);
+              tmem_st32(lane_base + uint32_t(ab * p.buf_cols + b * p.n_tile + gg * 32), v);
             }
           }
         }
@@ -1008,11 +1045,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_before();
       mbar_arrive(smem_u32(&acc_empty[ab]));
     };
-    init_buffer(blockIdx.x, 0);
-    if (p.nbuf == 2) init_buffer(blockIdx.x + gridDim.x, 1);
-    int it = 0;
+    for (int i = 0; i < p.nbuf; ++i) init_buffer(blockIdx.x + i * gridDim.x, i);
+    int it = 0, ab = 0, aph = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-      const int ab = p.nbuf == 2 ? (it & 1) : 0;
       const Tile tl = decode_tile(p, t);
       // a conv tile is one run of its N tile's groups: no shared-memory table
       // reads on the epilogue path (they queue behind the tensor core's
@@ -1022,7 +1057,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #ifdef MBU_TIMELINE
       unsigned long long te0 = clock64();
 #endif
-      if constexpr (!BLOCK_COMMIT) mbar_wait(smem_u32(&acc_full[ab]), (p.nbuf == 2 ? (it >> 1) : it) & 1);
+      if constexpr (!BLOCK_COMMIT) mbar_wait(smem_u32(&acc_full[ab]), aph);
 #ifdef MBU_TIMELINE
       unsigned long long te1 = clock64();
 #endif
@@ -1031,7 +1066,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       EPI_T(6);
       const int jt = tl.nt * p.n_tile;
       // units (block b, run ri): by block parity when MB >= 2, else by run parity
-      const bool split_b = !TCONV || p.MB >= 2;  // (a conv's N tile <= 128: MB >= 2)
+      const bool split_b = !TCONV || p.MB >= 2;
       for (int b = split_b ? half : 0; b < p.MB; b += split_b ? 2 : 1) {
         // this lane's pixel in block b, once per block
         const int q = block_q0(p, b) + m;
@@ -1042,7 +1077,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool valid = r >= 0 && r < p.R && c >= 0 && c < p.TW && yy < p.h && xx < p.w;
         const int64_t pix0 = TCONV ? (int64_t(tl.nb) * p.ho + yy * p.tconv_s) * p.wo + xx * p.tconv_s
                                    : (int64_t(tl.nb) * p.ho + yy) * p.wo + xx;
-        const uint32_t colb = lane_base + uint32_t(ab * ACC_COLS + b * p.n_tile);
+        const uint32_t colb = lane_base + uint32_t(ab * p.buf_cols + b * p.n_tile);
         if constexpr (BLOCK_COMMIT) {  // single buffer: one use per tile
           mbar_wait(smem_u32(&acc_full[b]), it & 1);
           tc_fence_after();
@@ -1110,6 +1145,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 p.bits[opix * p.out_stride32 + p.out_off32 + i] = 0u;
             continue;
           }
+          if (b == 0) EPI_T(13);
           if (valid && p.bits) {
             // write the run; when it ends the pixel's channels append the zero
             // pad groups of the 128-lane block (w8 is zero past the run)
@@ -1128,11 +1164,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int i = 8; i < cnt; ++i) dst[g0 + i] = 0u;
             }
           }
+          if (b == 0) EPI_T(14);
         }
       }
       EPI_T(10);
       // buffer drained: re-arm it with the bias of the tile that reuses it
       init_buffer(t + p.nbuf * gridDim.x, ab);
+      if (++ab == p.nbuf) {
+        ab = 0;
+        aph ^= 1;
+      }
       EPI_T(11);
 #ifdef MBU_TIMELINE
       if (blockIdx.x == 0 && lane == 0 && it < 64 && warp == 0) {
@@ -1563,7 +1604,15 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   // stream from L2; the un-overlapped epilogue costs a fraction of such a tile
   // (N = 64 long-K layers too: 7 blocks per tile with per-block commits, -2% on up-C3.a)
   p.nbuf = (fp4 && cv->kp >= 4 && (cv->n_tile == 128 || cv->n_tile == 64)) ? 1 : 2;
-  p.MB = fp4 ? std::min(8, (p.nbuf == 1 ? 2 * tc::FP4_COLS + 8 : tc::FP4_COLS) / cv->n_tile)
+  // three accumulator buffers of 2 blocks (N = 64) / 1 block (N = 128): the
+  // epilogue of a tile then overlaps two later tiles' MMAs
+  // (default: the one-K-stage N = 64 layers, measured -4% on stem2 / up-C3.b / up-C4.b;
+  // the two-stage up-C4.a loses 13% with it. MBU_NBUF3=0/1 forces it off / on where eligible)
+  static const int nbuf3 = std::getenv("MBU_NBUF3") ? std::atoi(std::getenv("MBU_NBUF3")) : -1;
+  if (fp4 && p.nbuf == 2 && (cv->n_tile == 64 || cv->n_tile == 128) &&
+      (nbuf3 > 0 || (nbuf3 < 0 && cv->n_tile == 64 && cv->kp == 1)))
+    p.nbuf = 3;
+  p.MB = fp4 ? std::min(8, (p.nbuf == 1 ? 2 * tc::FP4_COLS + 8 : p.nbuf == 3 ? 168 : tc::FP4_COLS) / cv->n_tile)
              : std::min(cv->taps == 9 ? 8 : 4, tc::ACC_COLS / cv->n_tile);  // one tap: Q <= 512
   if (x.w >= 128) {
     p.row_mode = 1;
@@ -1580,6 +1629,7 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
     p.col_tiles = 1;
   }
   p.p_magic = uint32_t((0x100000000ull + p.P - 1) / p.P);
+  p.buf_cols = fp4 && p.nbuf != 2 ? p.MB * cv->n_tile : tc::ACC_COLS;
   p.row_tiles = (x.h + p.R - 1) / p.R;
   const int q_last = p.row_mode ? (p.MB - 1 + p.halo) * p.P + p.halo
                                 : p.halo * p.P + p.halo + tc::BLOCK_M * (p.MB - 1);

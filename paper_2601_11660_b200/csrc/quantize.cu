@@ -19,7 +19,8 @@
 namespace mbu {
 namespace {
 
-__global__ void __launch_bounds__(256) quantize_kernel(const float *__restrict__ w, int64_t n, int binary,
+template <typename T>  // float32 or float64 weights, compared in float64 (numpy's promotion)
+__global__ void __launch_bounds__(256) quantize_kernel(const T *__restrict__ w, int64_t n, int binary,
                                                        double delta, int8_t *__restrict__ out) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const double v = double(w[i]);
@@ -78,14 +79,24 @@ __global__ void __launch_bounds__(128) fuse_bn_sign_kernel(const double *__restr
 }  // namespace
 }  // namespace mbu
 
-extern "C" int mbu_quantize_weights(const float *w, int64_t n, int binary, double delta, int8_t *out,
-                                    void *stream) {
+template <typename T>
+static int quantize_weights(const T *w, int64_t n, int binary, double delta, int8_t *out, void *stream) {
   using namespace mbu;
   if (n < 0) return fail(MBU_ERR_SHAPE, "quantize_weights: negative size");
   if (n == 0) return MBU_OK;
   const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
-  quantize_kernel<<<unsigned(blocks), 256, 0, as_stream(stream)>>>(w, n, binary, delta, out);
+  quantize_kernel<T><<<unsigned(blocks), 256, 0, as_stream(stream)>>>(w, n, binary, delta, out);
   return check_launch("quantize_kernel");
+}
+
+extern "C" int mbu_quantize_weights(const float *w, int64_t n, int binary, double delta, int8_t *out,
+                                    void *stream) {
+  return quantize_weights(w, n, binary, delta, out, stream);
+}
+
+extern "C" int mbu_quantize_weights_f64(const double *w, int64_t n, int binary, double delta, int8_t *out,
+                                        void *stream) {
+  return quantize_weights(w, n, binary, delta, out, stream);
 }
 
 extern "C" int mbu_fuse_bn_sign(const double *gamma, const double *beta, const double *mean, const double *var,

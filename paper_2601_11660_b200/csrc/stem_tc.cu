@@ -292,7 +292,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + 384);
   float *xm = reinterpret_cast<float *>(smem + 512);  // [XRING][NUM_PROD_WARPS]
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // (warp index through a shuffle: ptxas then treats it as warp-uniform, see conv_tc.cu)
+  const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < NA; ++i) {
       mbar_init(smem_u32(&full[i]), PROD_THREADS);

@@ -408,10 +408,14 @@ def quantize_weights(w, state: str, ternary_t: float = 0.7, *, device=None) -> n
         delta = float(ternary_t * np.abs(w).mean(dtype=np.float64))
     dev = cuda_device(device)
     with torch.cuda.device(dev):
-        src = torch.from_numpy(np.ascontiguousarray(w, dtype=np.float32)).to(dev)
+        # float32 stays float32 on the wire; anything else (float64, float16, ints) is
+        # widened exactly to float64 -- the kernel compares in float64 either way, as
+        # numpy does against the float64 delta (no narrowing, e.g. -1e-50 keeps its sign)
+        f32 = w.dtype == np.float32
+        src = torch.from_numpy(np.ascontiguousarray(w, dtype=np.float32 if f32 else np.float64)).to(dev)
         out = torch.empty(src.shape, dtype=torch.int8, device=dev)
-        _lib.call("mbu_quantize_weights", _ptr(src), src.numel(), 0 if state == MASKED_STATE else 1,
-                  delta, _ptr(out), _stream(dev))
+        _lib.call("mbu_quantize_weights" if f32 else "mbu_quantize_weights_f64", _ptr(src), src.numel(),
+                  0 if state == MASKED_STATE else 1, delta, _ptr(out), _stream(dev))
         return out.cpu().numpy()
 
 

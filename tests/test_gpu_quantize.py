@@ -57,6 +57,21 @@ def test_quantize_weights_gpu(cuda, rng):
     assert np.array_equal(ops.quantize_weights(tern, "masked", 0.7), tern.astype(np.int8))
 
 
+def test_quantize_weights_gpu_float64(cuda, rng):
+    # float64 weights are compared in float64 (no float32 narrowing): values that
+    # underflow or round across delta in float32 keep the host's decision
+    w = rng.standard_normal((32, 3, 3, 16))
+    w.flat[0], w.flat[1], w.flat[2] = -1e-50, 1e-50, -0.0
+    delta = 0.7 * np.abs(w).mean(dtype=np.float64)
+    w.flat[3] = np.nextafter(delta, np.inf)   # rounds to float32(delta) or below
+    w.flat[4] = np.nextafter(-delta, -np.inf)
+    for state in ("masked", "binary"):
+        want = quantizer.ternarize_values(w, 0.7) if state == "masked" else quantizer.binarize_values(w)
+        got = ops.quantize_weights(w, state, 0.7)
+        assert np.array_equal(got, want), state
+    assert ops.quantize_weights(w, "binary")[0, 0, 0, 0] == -1  # sign(-1e-50) = -1
+
+
 @pytest.mark.parametrize("gen,seed", [("synth", 3), ("live", 4)])
 def test_quantize_bundle_gpu_equals_host(cuda, gen, seed):
     cfg = tiny_config(extent=32, precision=mb.PrecisionMap.from_config_id(seed * 1237 % 4096))

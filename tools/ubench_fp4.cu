@@ -225,6 +225,55 @@ __global__ void fp4_mma_strip(int n, int q, int reps, int noise, unsigned long l
       for (int i = 0; i < 16; ++i) acc += v[i];
     }
     if (acc == 0x12345678u) clk[gridDim.x + blockIdx.x] = acc;
+  } else if (warp >= 4 && noise == 6) {
+    // ALU-bound warps (the epilogue's funnel-shift packing), until the MMAs finish:
+    // do they starve the MMA-issuing warp of issue slots?
+    uint32_t a0 = threadIdx.x, a1 = a0 * 3u, a2 = a0 * 5u, a3 = a0 * 7u;
+    while (!stop) {
+#pragma unroll 16
+      for (int j = 0; j < 64; ++j) {
+        a0 = __funnelshift_l(a1, a0, 1);
+        a1 = __funnelshift_l(a2, a1, 1);
+        a2 = __funnelshift_l(a3, a2, 1);
+        a3 = __funnelshift_l(a0, a3, 1);
+      }
+    }
+    if ((a0 ^ a1 ^ a2 ^ a3) == 0x12345678u) clk[gridDim.x + blockIdx.x] = a0;
+  } else if (warp >= 4 && warp < 8 && (noise == 4 || noise == 5)) {
+    // tcgen05.ld.32x32b.x64 + wait::ld latency of one epilogue-sized load (64 columns of
+    // the upper TMEM half) while the MMAs stream (4: until they finish) or with the
+    // tensor core idle (5: 2000 loads, reps = 0)
+    const uint32_t lq = tmem + (uint32_t((warp & 3) * 32) << 16) + 256u;
+    unsigned long long tot = 0;
+    unsigned cnt = 0, acc = 0;
+    while (noise == 4 ? !stop : cnt < 2000) {
+      uint32_t v[64];
+      const unsigned long long t0 = clock64();
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+          "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+          "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+            "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+            "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+            "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]),
+            "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]),
+            "=r"(v[38]), "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]),
+            "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]),
+            "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]),
+            "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]),
+            "=r"(v[62]), "=r"(v[63])
+          : "r"(lq));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      tot += clock64() - t0;
+      ++cnt;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) acc ^= v[i];
+    }
+    if (warp == 4 && (threadIdx.x & 31) == 0) clk[gridDim.x + blockIdx.x] = (tot / (cnt ? cnt : 1)) | (acc & 1ull) << 63;
   } else if (warp >= 4 && noise) {
     // 16-B stores over a 32 KB scratch region (bandwidth hog), until the MMAs finish
     uint4 *sc = reinterpret_cast<uint4 *>(scratch);
@@ -324,6 +373,23 @@ int main() {
         if (e != cudaSuccess) { printf("{\"error\": \"%s\"}\n", cudaGetErrorString(e)); return 1; }
         printf("{\"bench\": \"mxf4_strip\", \"n\": %d, \"mode\": %d, \"smem_store_noise\": %d, \"clk_per_mma\": %.1f}\n", n, mode, noise,
                double(ck[0]) / (27 * 300));
+      }
+    // MMA issue under ALU-bound co-resident warps (noise 6)
+    for (int n : {64, 128}) {
+      fp4_mma_strip<<<sms, 512, 200 * 1024>>>(n, 656, 27 * 300, 6, dclk, 2);
+      unsigned long long ck[148];
+      cudaMemcpy(ck, dclk, sms * 8, cudaMemcpyDeviceToHost);
+      printf("{\"bench\": \"mxf4_strip_alu_noise\", \"n\": %d, \"clk_per_mma\": %.1f}\n", n, double(ck[0]) / (27 * 300));
+    }
+    // TMEM load latency (epilogue-sized x64 load + wait) under a streaming MMA queue vs idle
+    for (int n : {64, 128})
+      for (int noise : {4, 5}) {
+        fp4_mma_strip<<<sms, 512, 200 * 1024>>>(n, 656, noise == 4 ? 27 * 300 : 0, noise, dclk, 2);
+        unsigned long long ck[2 * 148];
+        cudaError_t e = cudaMemcpy(ck, dclk, 2 * sms * 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) { printf("{\"error\": \"%s\"}\n", cudaGetErrorString(e)); return 1; }
+        printf("{\"bench\": \"tmem_ld_x64_latency\", \"n\": %d, \"mma_streaming\": %d, \"clk_per_ld\": %llu}\n", n,
+               int(noise == 4), ck[sms] & ~(1ull << 63));
       }
     cudaFree(dclk);
   }
