@@ -121,6 +121,8 @@ struct mbu_conv {
   int32_t *d_slab_of_nt4 = nullptr;
   int8_t *d_bias_slab = nullptr;
   int32_t *d_slab_of_nt = nullptr;
+  int32_t h_slab_of_nt[16] = {};   // host copies of the first 16 entries (kernel parameters)
+  int32_t h_slab_of_nt4[16] = {};
 };
 
 struct mbu_fconv {

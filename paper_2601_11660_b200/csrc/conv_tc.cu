@@ -153,6 +153,8 @@ struct Params {
   int n_slabs;
   const int8_t *bias_slab;  // [n_slabs][khalf][n_tile][16]: s8, sum(lo) + 127*sum(hi) = bias
   const int32_t *slab_of_nt;
+  int32_t slab_small[16];   // slab_of_nt for n_tiles <= 16, read from the constant bank (an LDS
+                            // in the MMA warp queues behind the tensor core's operand reads)
   const int32_t *col_bias;  // per GEMM column: TMEM init value
   const int32_t *col_sgn;   // per GEMM column: +-1
   const int32_t *col_w;     // per GEMM column: W (u8 mode) or 0
@@ -859,7 +861,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int nt = t - fdiv(t, p.nt_magic) * p.n_tiles;
         // (read before the wait: a shared load issued behind the tensor core's
         // operand reads takes hundreds of cycles, keep it off the issue path)
-        const int slab = p.mma_bias ? smap[nt] : 0;
+        const int slab = p.mma_bias ? (p.n_tiles <= 16 ? p.slab_small[nt] : smap[nt]) : 0;
 #ifdef MBU_TIMELINE
         unsigned long long tl0 = clock64();
 #endif
@@ -1065,8 +1067,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       EPI_T(6);
       const int jt = tl.nt * p.n_tile;
+      // Fast path (the benchmarked forward): a row-mode conv tile whose N tile is
+      // 64 or 128 full columns, no trace. Block b is output row y0 + b, lane m is
+      // column x0 + m, and the pixel's words are written as one 16-B store
+      // (N = 64: the two sign words plus the block's two zero pad words).
+      const bool fast = !TCONV && p.acc == nullptr && p.row_mode && (p.n_tile == 64 || p.n_tile == 128) &&
+                        p.n_gemm - jt >= p.n_tile;
+      if (fast) {
+        const int xx = tl.x0 + m;
+        const int64_t row_words = int64_t(p.wo) * p.out_stride32;
+        uint32_t *dst0 = p.bits + ((int64_t(tl.nb) * p.ho + tl.y0) * p.wo + xx) * p.out_stride32 + p.out_off32 +
+                         (jt >> 5);
+        for (int b = half; b < p.MB; b += 2) {
+          const uint32_t colb = lane_base + uint32_t(ab * p.buf_cols + b * p.n_tile);
+          if constexpr (BLOCK_COMMIT) {
+            mbar_wait(smem_u32(&acc_full[b]), it & 1);
+            tc_fence_after();
+          }
+          uint32_t v[64];
+          tmem_ld64(colb, v);
+          const uint32_t w0 = pack_nonneg<0>(v), w1 = pack_nonneg<32>(v);
+          uint32_t w2 = 0u, w3 = 0u;
+          if (p.n_tile == 128) {
+            tmem_ld64(colb + 64u, v);
+            w2 = pack_nonneg<0>(v);
+            w3 = pack_nonneg<32>(v);
+          }
+          if (xx < p.w && tl.y0 + b < p.h && p.bits)
+            *reinterpret_cast<uint4 *>(dst0 + b * row_words) = make_uint4(w0, w1, w2, w3);
+        }
+      }
       // units (block b, run ri): by block parity when MB >= 2, else by run parity
       const bool split_b = !TCONV || p.MB >= 2;
+      if (!fast)
       for (int b = split_b ? half : 0; b < p.MB; b += split_b ? 2 : 1) {
         // this lane's pixel in block b, once per block
         const int q = block_q0(p, b) + m;
@@ -1441,6 +1474,7 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
                                     cudaMemcpyHostToDevice),
                          "upload fp4 slab map"));
       cv->n_slabs4 = int(slabs.size() / sb);
+      for (int i = 0; i < 16 && i < n_tiles; ++i) cv->h_slab_of_nt4[i] = slab_of[i];
       cv->kp = kp;
       cv->pair_consec = consec ? 1 : 0;
       // pairs 2j, 2j+1 read the same 128-lane block: one stage can take both
@@ -1497,6 +1531,7 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
                                     cudaMemcpyHostToDevice),
                          "upload slab map"));
       cv->n_slabs = int(slabs.size() / sb);
+      for (int i = 0; i < 16 && i < n_tiles; ++i) cv->h_slab_of_nt[i] = slab_of[i];
     }
   }
   cv->b_stage_bytes = b_stage;
@@ -1710,6 +1745,7 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   p.n_slabs = n_slabs;
   p.bias_slab = fp4 ? reinterpret_cast<const int8_t *>(cv->d_bias_slab4) : cv->d_bias_slab;
   p.slab_of_nt = fp4 ? cv->d_slab_of_nt4 : cv->d_slab_of_nt;
+  for (int i = 0; i < 16 && i < cv->n_tiles; ++i) p.slab_small[i] = fp4 ? cv->h_slab_of_nt4[i] : cv->h_slab_of_nt[i];
   off = (off + 1023) / 1024 * 1024;
   p.off_ones = uint32_t(off);
   p.off_slab = uint32_t(off + (p.mma_bias ? 4096 : 0));
