@@ -1,0 +1,19 @@
+#!/bin/bash
+# A/B device timing of libraries (MBU_LIB=...), interleaved, after a clock-settling run:
+#   tools/ab_libs.sh build/ab/base.so build/ab/cur.so ...
+mkdir -p gpurun_out
+timeout 600 python bench.py --no-cpu --no-cudnn --no-e2e --steps 10 --warmup 5 > /dev/null 2>&1
+for rep in 1 2; do
+  for lib in "$@"; do
+    MBU_LIB=$lib timeout 600 python bench.py --no-cpu --no-cudnn --no-e2e --steps 20 --warmup 5 > gpurun_out/ab.json 2>gpurun_out/ab.err
+    python - "$lib" <<'PY'
+import json, sys
+try:
+    d = json.load(open("gpurun_out/ab.json"))
+except Exception:
+    print(sys.argv[1], "FAILED", open("gpurun_out/ab.err").read()[-800:]); raise SystemExit
+ks = {k["layer"]: k["ms"] for k in d["kernel_breakdown"]}
+print(f'{sys.argv[1]:22s} value {d["value"]:7.1f}  ' + " ".join(f'{n}={v:.3f}' for n, v in ks.items()))
+PY
+  done
+done
