@@ -1073,6 +1073,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // (N = 64: the two sign words plus the block's two zero pad words).
       const bool fast = !TCONV && p.acc == nullptr && p.row_mode && (p.n_tile == 64 || p.n_tile == 128) &&
                         p.n_gemm - jt >= p.n_tile;
+      // 2x2/s2 tconv whose N tile holds all four taps of <= 64 channels (up-CT4):
+      // half h writes output row 2y + h, both dx taps of a pixel as 32
+      // contiguous bytes (lanes: consecutive x), so every sector is written
+      // whole by one thread instead of two half-sector writes from two warps
+      const bool fast_t = TCONV && p.acc == nullptr && p.row_mode && p.tconv_s == 2 && p.c_out_pad == 64 &&
+                          p.n_tile == 256 && p.out_groups == 4 && p.bits;
+      if (fast_t) {
+        const int xx = tl.x0 + m;
+        for (int b = 0; b < p.MB; ++b) {
+          const int yy = tl.y0 + b;
+          const uint32_t colb = lane_base + uint32_t(ab * p.buf_cols + b * p.n_tile + 128 * half);
+          uint32_t v[64];
+          tmem_ld64(colb, v);  // tap (half, 0)
+          const uint32_t w0 = pack_nonneg<0>(v), w1 = pack_nonneg<32>(v);
+          tmem_ld64(colb + 64u, v);  // tap (half, 1)
+          const uint32_t w2 = pack_nonneg<0>(v), w3 = pack_nonneg<32>(v);
+          if (xx < p.w && yy < p.h) {
+            uint32_t *dst = p.bits + ((int64_t(tl.nb) * p.ho + 2 * yy + half) * p.wo + 2 * xx) * p.out_stride32 +
+                            p.out_off32;
+            *reinterpret_cast<uint4 *>(dst) = make_uint4(w0, w1, 0u, 0u);
+            *reinterpret_cast<uint4 *>(dst + p.out_stride32) = make_uint4(w2, w3, 0u, 0u);
+          }
+        }
+      }
       if (fast) {
         const int xx = tl.x0 + m;
         const int64_t row_words = int64_t(p.wo) * p.out_stride32;
@@ -1099,7 +1123,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       // units (block b, run ri): by block parity when MB >= 2, else by run parity
       const bool split_b = !TCONV || p.MB >= 2;
-      if (!fast)
+      if (!fast && !fast_t)
       for (int b = split_b ? half : 0; b < p.MB; b += split_b ? 2 : 1) {
         // this lane's pixel in block b, once per block
         const int q = block_q0(p, b) + m;
