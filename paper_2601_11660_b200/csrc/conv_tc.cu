@@ -1084,11 +1084,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int b = 0; b < p.MB; ++b) {
           const int yy = tl.y0 + b;
           const uint32_t colb = lane_base + uint32_t(ab * p.buf_cols + b * p.n_tile + 128 * half);
-          uint32_t v[64];
-          tmem_ld64(colb, v);  // tap (half, 0)
-          const uint32_t w0 = pack_nonneg<0>(v), w1 = pack_nonneg<32>(v);
-          tmem_ld64(colb + 64u, v);  // tap (half, 1)
-          const uint32_t w2 = pack_nonneg<0>(v), w3 = pack_nonneg<32>(v);
+          // (32-column loads: two live 64-register loads spill)
+          uint32_t v[32];
+          tmem_ld32(colb, v);  // tap (half, 0)
+          const uint32_t w0 = pack_nonneg<0>(v);
+          tmem_ld32(colb + 32u, v);
+          const uint32_t w1 = pack_nonneg<0>(v);
+          tmem_ld32(colb + 64u, v);  // tap (half, 1)
+          const uint32_t w2 = pack_nonneg<0>(v);
+          tmem_ld32(colb + 96u, v);
+          const uint32_t w3 = pack_nonneg<0>(v);
           if (xx < p.w && yy < p.h) {
             uint32_t *dst = p.bits + ((int64_t(tl.nb) * p.ho + 2 * yy + half) * p.wo + 2 * xx) * p.out_stride32 +
                             p.out_off32;
@@ -1108,14 +1113,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_wait(smem_u32(&acc_full[b]), it & 1);
             tc_fence_after();
           }
-          uint32_t v[64];
-          tmem_ld64(colb, v);
-          const uint32_t w0 = pack_nonneg<0>(v), w1 = pack_nonneg<32>(v);
+          uint32_t v[32];
+          tmem_ld32(colb, v);
+          const uint32_t w0 = pack_nonneg<0>(v);
+          tmem_ld32(colb + 32u, v);
+          const uint32_t w1 = pack_nonneg<0>(v);
           uint32_t w2 = 0u, w3 = 0u;
           if (p.n_tile == 128) {
-            tmem_ld64(colb + 64u, v);
+            tmem_ld32(colb + 64u, v);
             w2 = pack_nonneg<0>(v);
-            w3 = pack_nonneg<32>(v);
+            tmem_ld32(colb + 96u, v);
+            w3 = pack_nonneg<0>(v);
           }
           if (xx < p.w && tl.y0 + b < p.h && p.bits)
             *reinterpret_cast<uint4 *>(dst0 + b * row_words) = make_uint4(w0, w1, w2, w3);
