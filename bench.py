@@ -297,6 +297,249 @@ def _profile_traffic():
     return None
 
 
+# ----------------------------------------------------------------- configs 2 and 5
+
+C2_OPS = 19_327_352_832  # 2 * 128 * 128 * 256 * (9 * 256): SURVEY.md 8(d), config 2
+
+
+def config2_microbench(dev, reps=200):
+    """BASELINE config 2: one masked 3x3 conv, 256 -> 256 channels, 1 x 128 x 128, at
+    50 / 90 / 95 % weight sparsity (ternary weights, P(0) = s, non-zeros +-1).
+    Device time of the tcgen05 conv per call (CUDA events around a CUDA graph of
+    `reps` launches), once producing the reference's int32 accumulators
+    (conv_forward, layers.py:289-313) and once with the fused threshold + packed
+    bits the network runs; checked exactly against the CPU oracle first."""
+    import torch
+
+    import paper_2601_11660_b200 as mb
+    from oracle import engine as port
+    from paper_2601_11660_b200.ops import ConvHandle, _words_to_dev
+
+    rng = np.random.default_rng(0)
+    acts = (rng.integers(0, 2, (1, 128, 128, 256)) * 2 - 1).astype(np.int8)
+    x = mb.pack_tensor(acts)
+    spec = mb.ConvSpec(3, 3, 1, 1, 256, 256)
+    rows = []
+    xd = _words_to_dev(x.words, dev)
+    for sp in (0.5, 0.9, 0.95):
+        nz = rng.random((256, 3, 3, 256)) >= sp
+        w = np.where(nz, rng.choice((-1, 1), size=nz.shape), 0).astype(np.int8)
+        planes = mb.pack_conv_weights(w, x.segments, masked=True)
+        thr = mb.FusedThreshold(np.zeros(256, np.int32), np.zeros(256, np.uint8))
+        cv = ConvHandle(planes, spec, x.segments, thr, device=dev)
+        acc = torch.empty((1, 128, 128, 256), dtype=torch.int32, device=dev)
+        bits = torch.empty((1, 128, 128, cv.out_wpp), dtype=torch.int64, device=dev)
+        cv.run(xd, 1, 128, 128, acc=acc)
+        torch.cuda.synchronize(dev)
+        want = port.conv_forward(x.words, [(g.lane_offset, g.count) for g in x.segments], planes, spec, 8)
+        exact = bool(np.array_equal(acc.cpu().numpy(), want))
+        res = {"sparsity": sp, "exact_vs_oracle": exact}
+        for name, kw in (("acc_int32", {"acc": acc}), ("fused_threshold_bits", {"bits": bits})):
+            st = torch.cuda.Stream(dev)
+            with torch.cuda.stream(st):
+                for _ in range(3):
+                    cv.run(xd, 1, 128, 128, **kw)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    for _ in range(reps):
+                        cv.run(xd, 1, 128, 128, **kw)
+            times = []
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(st):  # (replay runs on the current stream)
+                    e0.record(st)
+                    g.replay()
+                    e1.record(st)
+                torch.cuda.synchronize(dev)
+                times.append(e0.elapsed_time(e1) / reps)
+            ms = statistics.median(times)
+            res[name] = {"us_per_conv": 1e3 * ms, "tops": C2_OPS / (ms / 1e3) / 1e12}
+        rows.append(res)
+    return {"workload": "config 2: masked 3x3 conv 256->256, 1x128x128, ternary weights",
+            "ops_per_conv": C2_OPS, "rows": rows,
+            "how": "CUDA graph of 200 back-to-back launches of the tcgen05 conv (ConvHandle.run), "
+                   "median of 5 replays; 16384 output pixels fill 128 of 148 SMs once, so this is a "
+                   "latency-bound size for one GPU"}
+
+
+def config2_reference_cpu():
+    """The reference's own micro_bench (bitunet.bench.micro_bench, bench.py:207-243) at
+    config 2's shape on this host, from the unmodified install in baseline/_ref."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "bitunet").is_dir():
+        return {"unavailable": "baseline/_ref not installed"}
+    code = f"""
+import json, os, sys
+sys.path.insert(0, {str(ref)!r})
+from bitunet.bench import micro_bench
+thr = len(os.sched_getaffinity(0))
+mb = micro_bench(channels=256, extent=128, kernel=3, reps=3, threads=thr, include_oracle=False)
+print(json.dumps({{"seconds": mb.t_bit, "threads": thr, "n_ops": mb.n_ops}}))
+"""
+    env = dict(os.environ, NUMBA_CACHE_DIR=os.environ.get("NUMBA_CACHE_DIR", "/tmp/mbu_numba_cache"),
+               PYTHONDONTWRITEBYTECODE="1", MBU_REFERENCE_ERRORS="0")
+    try:
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001 - a reported baseline only
+        return {"unavailable": f"micro_bench failed: {type(e).__name__}"}
+    return {"seconds_per_conv": d["seconds"], "gops": d["n_ops"] / d["seconds"] / 1e9, "threads": d["threads"],
+            "what": "bitunet.bench.micro_bench(channels=256, extent=128) conv_forward time (its own "
+                    "uniform ternary weights), Numba XOR-popcount path, all host threads"}
+
+
+def config5_latency(dev, frames=200):
+    """BASELINE config 5: 4K (3x2160x3840) batch-1 per-frame latency, p50/p99 over
+    `frames` frames: device (CUDA-graph replay, image resident) and end to end
+    (pinned float64 frame H2D + forward + uint8 mask and float64 logits D2H, one
+    stream, synchronised per frame)."""
+    import torch
+
+    import paper_2601_11660_b200 as mb
+    from paper_2601_11660_b200.quantizer import bench_frame
+
+    cfg = mb.UNetConfig(height=2160, width=3840)
+    model = mb.build(cfg, mb.live_bundle(cfg, np.random.default_rng(SEED)))
+    eng = mb.Engine(model, batch=1, device=dev)
+    host = torch.from_numpy(bench_frame(0, 2160, 3840)[None]).pin_memory()
+    hl = torch.empty(eng.out_shape, dtype=torch.float64, pin_memory=True)
+    hm = torch.empty(eng.out_shape, dtype=torch.uint8, pin_memory=True)
+    eng.image.copy_(host)
+    for _ in range(10):
+        eng.run()
+    torch.cuda.synchronize(dev)
+
+    def pct(v, q):
+        v = sorted(v)
+        return v[min(len(v) - 1, int(round(q * (len(v) - 1))))]
+
+    dev_ms, e2e_ms = [], []
+    for _ in range(frames):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(eng.stream)
+        eng.run()
+        e1.record(eng.stream)
+        e1.synchronize()
+        dev_ms.append(e0.elapsed_time(e1))
+    for _ in range(frames):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(eng.stream)
+        eng.run_e2e(host, hl, hm)
+        e1.record(eng.stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    ops = 7_648_365_772_800
+    out = {"workload": "config 5: MBU-Net 1x3x2160x3840, batch 1", "frames": frames,
+           "device_ms": {"p50": pct(dev_ms, 0.5), "p99": pct(dev_ms, 0.99), "min": min(dev_ms)},
+           "e2e_ms": {"p50": pct(e2e_ms, 0.5), "p99": pct(e2e_ms, 0.99), "min": min(e2e_ms)},
+           "device_tops_p50": ops / (pct(dev_ms, 0.5) / 1e3) / 1e12,
+           "h2d_bytes_per_frame": host.numel() * 8, "d2h_bytes_per_frame": hl.numel() * 8 + hm.numel(),
+           "how": "Engine (CUDA graph), CUDA events per frame on the engine stream; e2e = run_e2e "
+                  "(pinned image H2D, replay, logits + mask D2H) synchronised per frame"}
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
+STREAM = 64  # config 4: a 64-frame stream over the node's GPUs
+
+
+def run_multi(args):
+    """BASELINE config 4 (N > 1): a 64-frame 1024x2048 stream sharded contiguously
+    over the N ranks (dp.StreamRunner: 64/N frames each, batches of 8, no
+    collective on the data path), strong scaling. ``value``: device-resident
+    forwards of every rank's shard; ``e2e``: pinned 8-bit frames H2D, GPU decode,
+    forward, GPU-packed masks, and the final gather of all packed masks to rank 0
+    (NCCL) plus its D2H. Both timed on the device, max over ranks."""
+    import torch
+
+    import paper_2601_11660_b200 as mb
+    from paper_2601_11660_b200 import _lib, dp
+
+    dist, rank, world, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    cfg = _config()
+    model = _model(cfg)
+    runner = dp.StreamRunner(model, STREAM, batch=BATCH, dist=dist, device=dev)
+    eng = runner.engine
+    eng.image.copy_(torch.from_numpy(_frames(runner.lo)))
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    clocks = ClockSampler(local)
+    for _ in range(args.warmup):
+        runner.run_resident()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    before = _lib.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(eng.stream)
+    for _ in range(args.steps):
+        runner.run_resident()
+    e1.record(eng.stream)
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - before
+    dist.barrier()
+    dev_ms = max_over_ranks(e0.elapsed_time(e1))
+    value = STREAM * args.steps / (dev_ms / 1e3)
+
+    e2e = None
+    if not args.no_e2e:
+        g = torch.Generator().manual_seed(77 + rank)
+        raster = torch.randint(0, 256, (runner.n_local, H, W, 3), dtype=torch.uint8, generator=g).pin_memory()
+        for _ in range(args.warmup):
+            runner.run(raster)
+            runner.gather(0)
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        eng._ensure_slots()
+        h0.record(eng.h2d)
+        for _ in range(args.steps):
+            runner.run(raster)
+            runner.gather(0)
+        h1.record(torch.cuda.current_stream(dev))
+        torch.cuda.synchronize()
+        dist.barrier()
+        e2e_ms = max_over_ranks(h0.elapsed_time(h1))
+        e2e = {"value": STREAM * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": STREAM * H * W * 3,
+               "d2h_bytes_per_step": STREAM * ((H * W + 7) // 8),
+               "ms_per_step": e2e_ms / args.steps,
+               "how": "dp.StreamRunner per rank: pinned 8-bit frames H2D (copy stream), "
+                      "decode_raster + CUDA-graph forward + pack_mask_bits on the GPU, then "
+                      "gather of every rank's bit-packed masks to rank 0 (NCCL) and D2H there"}
+    clk = clocks.stop()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "e2m1 (tcgen05 kind::mxf4, exact f32 integer acc) 3x3 convs / s8 tconvs / "
+                     "u64 bitplanes / f64 endpoints",
+            "data": "synthetic: live-generator random weights (seed 0), bench_frame images "
+                    "(resident), random 8-bit frames (e2e)",
+            "config": {"workload": f"config 4: MBU-Net 64-frame 3x1024x2048 stream over {world} GPUs "
+                                   f"({STREAM // world} frames each, batches of {BATCH})",
+                       "global_batch": STREAM, "height": H, "width": W,
+                       "parallelism": f"dp{world} (frame shards, no data-path collective)",
+                       "l2": "inputs and activations larger than L2"},
+            "e2e": e2e, "roofline": None, "cpu_baseline": None, "clocks": clk,
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
 def run_ours(args):
     import torch
 
@@ -494,6 +737,18 @@ def run_ours(args):
         if not args.no_cpu and world == 1:
             cpu = cpu_baseline(model)
             numba = cpu_numba_baseline(cfg)
+        c2 = c5 = None
+        if not args.no_extra and world == 1:
+            try:
+                c2 = config2_microbench(dev)
+                if not args.no_cpu:
+                    c2["reference_cpu"] = config2_reference_cpu()
+            except Exception as e:  # noqa: BLE001 - extra keys must not sink the headline line
+                c2 = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+            try:
+                c5 = config5_latency(dev)
+            except Exception as e:  # noqa: BLE001
+                c5 = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
@@ -514,6 +769,8 @@ def run_ours(args):
             "clocks": clk,
             "gpu_launches": eng.launches_per_run * args.steps,
             "kernel_breakdown": breakdown,
+            "config2_microbench": c2,
+            "config5_4k_latency": c5,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -531,11 +788,14 @@ def main(argv=None):
     ap.add_argument("--no-cudnn", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config 2 / config 5 keys")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_multi(args)
     return run_ours(args)
 
 

@@ -149,6 +149,13 @@ int mbu_fconv_run(mbu_fconv *conv, const double *x_f64, const uint64_t *x_bits,
 int mbu_argmax(const double *logits, int64_t pixels, int channels, uint8_t *classes,
                void *stream);
 
+/* Bit-packed masks for the multi-GPU host gather (an
+ * extra): per frame, packed[f][k] bit j = mask[f][8k + j] & 1
+ * (numpy.packbits(mask[f].ravel(), bitorder="little")); per_frame = H*W*C
+ * mask bytes, ceil(per_frame / 8) packed bytes per frame. */
+int mbu_pack_mask(const uint8_t *mask, int64_t frames, int64_t per_frame, uint8_t *packed,
+                  void *stream);
+
 /* Netpbm raster -> float64 image (imageio.py:59-83 read_image): out[i] =
  * sample[i] / maxval, samples u8 (bytes_per_sample 1) or big-endian u16 (2),
  * the same correctly rounded float64 division as the reference. */

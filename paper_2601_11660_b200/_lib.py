@@ -35,6 +35,7 @@ _SIGS = {
     "mbu_last_path": (_i, []),
     "mbu_set_option": (_i, [_i, _i]),
     "mbu_argmax": (_i, [_vp, _i64, _i, _vp, _vp]),
+    "mbu_pack_mask": (_i, [_vp, _i64, _i64, _vp, _vp]),
     "mbu_decode_raster": (_i, [_vp, _i64, _i, _i, _vp, _vp]),
     "mbu_quantize_weights": (_i, [_vp, _i64, _i, _c.c_double, _vp, _vp]),
     "mbu_quantize_weights_f64": (_i, [_vp, _i64, _i, _c.c_double, _vp, _vp]),

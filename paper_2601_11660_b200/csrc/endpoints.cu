@@ -370,6 +370,43 @@ extern "C" int mbu_argmax(const double *logits, int64_t pixels, int channels, ui
 }
 
 // ---------------------------------------------------------------------------
+// bit-packed masks for the multi-GPU gather (dp.py): one bit
+// per mask byte, numpy.packbits(..., bitorder="little") per frame
+// ---------------------------------------------------------------------------
+namespace mbu {
+__global__ void __launch_bounds__(256) pack_mask_kernel(const uint8_t *__restrict__ mask, int64_t frames,
+                                                        int64_t per_frame, int64_t out_per_frame,
+                                                        uint8_t *__restrict__ out) {
+  const int64_t total = frames * out_per_frame;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t f = i / out_per_frame, k = i - f * out_per_frame;
+    const uint8_t *src = mask + f * per_frame + 8 * k;
+    const int64_t left = per_frame - 8 * k;
+    uint32_t b = 0;
+    if (left >= 8 && (reinterpret_cast<uintptr_t>(src) & 7) == 0) {
+      const uint2 v = __ldg(reinterpret_cast<const uint2 *>(src));
+      // (x & 0x01010101) * 0x01020408: byte j's bit 0 lands at bit 24 + j
+      b = (((v.x & 0x01010101u) * 0x01020408u) >> 24) | ((((v.y & 0x01010101u) * 0x01020408u) >> 24) << 4);
+    } else {
+      for (int j = 0; j < 8 && j < left; ++j) b |= uint32_t(src[j] & 1u) << j;
+    }
+    out[i] = uint8_t(b);
+  }
+}
+}  // namespace mbu
+
+extern "C" int mbu_pack_mask(const uint8_t *mask, int64_t frames, int64_t per_frame, uint8_t *packed,
+                             void *stream) {
+  using namespace mbu;
+  if (frames < 0 || per_frame < 0) return fail(MBU_ERR_SHAPE, "pack_mask: negative size");
+  const int64_t out_per_frame = (per_frame + 7) / 8, total = frames * out_per_frame;
+  if (total == 0) return MBU_OK;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
+  pack_mask_kernel<<<unsigned(blocks), 256, 0, as_stream(stream)>>>(mask, frames, per_frame, out_per_frame, packed);
+  return check_launch("pack_mask_kernel");
+}
+
+// ---------------------------------------------------------------------------
 // netpbm raster -> float64 image (imageio.py:59-83): sample / maxval
 // ---------------------------------------------------------------------------
 namespace mbu {

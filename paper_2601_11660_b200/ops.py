@@ -360,6 +360,24 @@ def argmax_classes(logits, *, device=None):
     return out if on_dev else out.cpu().numpy()
 
 
+def pack_mask_bits(mask, *, out=None):
+    """Bit-pack a device uint8 mask (n, ...) per frame on the GPU (``mbu_pack_mask``):
+    the result row f equals ``numpy.packbits(mask[f].ravel(), bitorder="little")``
+    (1 bit per pixel: 256 KB per 1024x2048 frame instead of 2 MB)."""
+    if not (isinstance(mask, torch.Tensor) and mask.is_cuda and mask.dtype == torch.uint8):
+        raise ShapeError("pack_mask_bits takes a uint8 CUDA tensor")
+    m = mask.contiguous()
+    n = m.shape[0]
+    per = m[0].numel() if n else 0
+    if out is None:
+        out = torch.empty((n, (per + 7) // 8), dtype=torch.uint8, device=m.device)
+    elif tuple(out.shape) != (n, (per + 7) // 8) or out.dtype != torch.uint8 or not out.is_contiguous():
+        raise ShapeError(f"packed output must be contiguous uint8 {(n, (per + 7) // 8)}")
+    with torch.cuda.device(m.device):
+        _lib.call("mbu_pack_mask", _ptr(m), n, per, _ptr(out), _stream(m.device))
+    return out
+
+
 def decode_raster(raster, maxval: int, *, out=None, device=None):
     """Netpbm samples -> float64 image on the GPU (``mbu_decode_raster``):
     ``sample / maxval``, bit-identical to ``read_image`` / the reference's

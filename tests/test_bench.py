@@ -39,3 +39,6 @@ def test_our_arm_line():
     r = d["roofline"]
     assert r["bound"] == "tensor" and 0 < r["frac"] < 1 and r["achieved"] > 0 and r["peak"] > 0
     assert d["gpu_launches"] > 0
+    c2, c5 = d["config2_microbench"], d["config5_4k_latency"]
+    assert all(r["exact_vs_oracle"] and r["fused_threshold_bits"]["tops"] > 0 for r in c2["rows"])
+    assert c5["frames"] >= 200 and 0 < c5["device_ms"]["p50"] <= c5["device_ms"]["p99"]

@@ -1,11 +1,12 @@
-"""Data-parallel sharding and the final gather, world size 2 over gloo (CPU).
+"""Data-parallel sharding and the final gather, world size 2 (and 3) over gloo (CPU).
 
 The B200 path shards frames across ranks with no collective on the data path
-(SURVEY.md §8(e)); the only exchange is the result gather to rank 0. Here the
-per-rank forward is the CPU engine port (oracle/engine.py) standing in for a
-rank's GPU Engine, so the sharding + packing + gather logic is checked
-end to end without a GPU: gathered masks and logits must equal one
-process's forward over the whole stream, frame for frame.
+(SURVEY.md §8(e)); the only exchange is the result gather to rank 0. These
+tests drive the runner's own sharding / gather class (``dp.ShardedStream``,
+the base of ``dp.StreamRunner``) with the CPU engine port (oracle/engine.py)
+standing in for a rank's GPU forward: the gathered bit-packed masks (and
+logits through ``gather_frames``) must equal one process's forward over the
+whole stream, frame for frame. ``tests/test_gpu_dp.py`` runs the GPU runner.
 """
 
 from __future__ import annotations
@@ -47,13 +48,17 @@ def _worker(rank, world, port, out_path):
         from oracle import engine
 
         model, frames = _stream()
-        a, b = dp.shard_bounds(N_FRAMES, world, rank)
+        cfg = model.config
+        sh = dp.ShardedStream(N_FRAMES, cfg.height * cfg.width * cfg.out_channels, dist=dist)
+        a, b = sh.lo, sh.hi
+        assert (a, b) == dp.shard_bounds(N_FRAMES, world, rank)
         logits, mask, _ = engine.forward(model, frames[a:b])
-        packed = torch.from_numpy(dp.pack_masks(mask))
-        got_mask = dp.gather_frames(packed, N_FRAMES, dist)
+        if sh.n_local:
+            sh.packed[:sh.n_local] = torch.from_numpy(dp.pack_masks(mask))
+        got_mask = sh.gather(dst=0)
         got_logits = dp.gather_frames(torch.from_numpy(logits), N_FRAMES, dist)
         if rank == 0:
-            np.savez(out_path, mask=dp.unpack_masks(got_mask.numpy(), mask.shape),
+            np.savez(out_path, mask=dp.unpack_masks(got_mask, (N_FRAMES,) + mask.shape[1:]),
                      logits=got_logits.numpy())
         else:
             assert got_mask is None and got_logits is None
@@ -80,11 +85,12 @@ def test_pack_masks_round_trip(rng):
     assert np.array_equal(dp.unpack_masks(p, m.shape), m)
 
 
-def test_two_rank_gloo_shard_and_gather_equals_single_process(tmp_path):
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_shard_and_gather_equals_single_process(tmp_path, world):
     from oracle import engine
 
     out = tmp_path / "gathered.npz"
-    mp.spawn(_worker, args=(2, _free_port(), str(out)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(out)), nprocs=world, join=True)
     model, frames = _stream()
     logits, mask, _ = engine.forward(model, frames)
     got = np.load(out)

@@ -2,10 +2,10 @@
 # A/B device timing of libraries (MBU_LIB=...), interleaved, after a clock-settling run:
 #   tools/ab_libs.sh build/ab/base.so build/ab/cur.so ...
 mkdir -p gpurun_out
-timeout 600 python bench.py --no-cpu --no-cudnn --no-e2e --steps 10 --warmup 5 > /dev/null 2>&1
+timeout 600 python bench.py --no-cpu --no-cudnn --no-e2e --no-extra --steps 10 --warmup 5 > /dev/null 2>&1
 for rep in 1 2; do
   for lib in "$@"; do
-    MBU_LIB=$lib timeout 600 python bench.py --no-cpu --no-cudnn --no-e2e --steps 20 --warmup 5 > gpurun_out/ab.json 2>gpurun_out/ab.err
+    MBU_LIB=$lib timeout 600 python bench.py --no-cpu --no-cudnn --no-e2e --no-extra --steps 20 --warmup 5 > gpurun_out/ab.json 2>gpurun_out/ab.err
     python - "$lib" <<'PY'
 import json, sys
 try:
