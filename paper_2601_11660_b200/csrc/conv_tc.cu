@@ -504,7 +504,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t *bres = acc_empty + 4;  // resident weights landed
   uint64_t *rfull = bres + 1;       // [8] FP4: raw box landed (TMA)
   uint64_t *rempty = rfull + 8;     // [8] FP4: raw box consumed (producers)
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rempty + 8);
+  uint64_t *sf_ready = rempty + 8;  // FP4: the block-scale TMEM columns are written
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sf_ready + 1);
   int32_t *chunk_s = reinterpret_cast<int32_t *>(smem + 512);  // MAX_CHUNKS words
   uint8_t *a_base = smem + SMEM_HEADER;
   uint8_t *b_base = smem + p.off_b;
@@ -525,6 +526,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int i = 0; i < 8; ++i) {
       mbar_init(smem_u32(&rfull[i]), 1);
       mbar_init(smem_u32(&rempty[i]), PROD_THREADS);
+    }
+    {
+      mbar_init(smem_u32(sf_ready), 128);
     }
     for (int i = 0; i < 8; ++i) mbar_init(smem_u32(&acc_full[i]), 1);
     for (int i = 0; i < 3; ++i) mbar_init(smem_u32(&acc_empty[i]), EPI_THREADS);
@@ -585,9 +589,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
-      asm volatile("bar.sync 1, 160;" ::: "memory");
-    } else if (warp == MMA_WARP) {
-      asm volatile("bar.sync 1, 160;" ::: "memory");
+      mbar_arrive(smem_u32(sf_ready));  // (an mbarrier rather than a partial named
+    } else if (warp == MMA_WARP) {      //  barrier: compute-sanitizer synccheck clean)
+      mbar_wait(smem_u32(sf_ready), 0);
       tc_fence_after();
     }
   }
