@@ -283,6 +283,45 @@ __global__ void __launch_bounds__(256) head_tab_kernel(ActView xb, const double 
   }
 }
 
+// The default network's head (c_out = 1, 64 input channels = two words per
+// pixel, a plain tensor): bandwidth-shaped. Each thread takes four pixels
+// a block-width apart (every warp load / store instruction covers
+// consecutive pixels), issues their 16-B loads first, then runs four
+// independent table-lookup chains in head_tab_kernel's order.
+__global__ void __launch_bounds__(256) head_tab64_kernel(const uint4 *__restrict__ x, const double *__restrict__ tab,
+                                                         const double *__restrict__ bias, int64_t pixels,
+                                                         double *__restrict__ logits, uint8_t *__restrict__ mask) {
+  __shared__ double ts[8 * 256];
+  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) ts[i] = tab[i];
+  __syncthreads();
+  const double b0 = bias ? __ldg(bias) : 0.0;
+  const int64_t chunk = int64_t(blockDim.x) * 4;
+  for (int64_t base = int64_t(blockIdx.x) * chunk; base < pixels; base += int64_t(gridDim.x) * chunk) {
+    uint4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t q = base + j * blockDim.x + threadIdx.x;
+      v[j] = q < pixels ? __ldcs(x + q) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t q = base + j * blockDim.x + threadIdx.x;
+      const uint32_t w[2] = {v[j].x, v[j].y};  // channels 0-63 (z, w: the block's pad lanes)
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t word = k < 4 ? w[0] : w[1];
+        acc = __dadd_rn(acc, ts[k * 256 + int((word >> (8 * (k & 3))) & 0xFFu)]);
+      }
+      if (bias) acc = __dadd_rn(acc, b0);
+      if (q < pixels) {
+        __stcs(logits + q, acc);
+        if (mask) mask[q] = acc >= 0.0 ? 1 : 0;
+      }
+    }
+  }
+}
+
 int head_prepare(mbu_fconv *fc, const double *w, const int32_t *lanes) {
   fc->head_tab = 0;
   if (!(fc->bits_input && fc->kh == 1 && fc->kw == 1 && fc->stride == 1 && fc->pad == 0)) return MBU_OK;
@@ -313,6 +352,13 @@ int launch_head_fast(const mbu_fconv *fc, const ActView &xb, int n, int h, int w
                      uint8_t *mask, cudaStream_t st) {
   const int64_t pixels = int64_t(n) * h * w;
   if (pixels == 0) return MBU_OK;
+  if (fc->head_tab && fc->c_out == 1 && (fc->c_in + 7) / 8 == 8 && xb.stride == 2 && xb.offset == 0 &&
+      !xb.split && (reinterpret_cast<uintptr_t>(xb.base) & 15) == 0) {
+    const int64_t blocks = std::min<int64_t>((pixels + 1023) / 1024, 148 * 8);
+    head_tab64_kernel<<<unsigned(blocks), 256, 0, st>>>(reinterpret_cast<const uint4 *>(xb.base), fc->d_head_tab,
+                                                        fc->d_bias, pixels, logits, mask);
+    return check_launch("head_tab64_kernel");
+  }
   if (fc->head_tab) {
     const int nbytes = (fc->c_in + 7) / 8;
     const size_t smem = size_t(fc->c_out) * nbytes * 256 * sizeof(double);
