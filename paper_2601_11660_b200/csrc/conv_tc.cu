@@ -1675,6 +1675,19 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   // stream from L2; the un-overlapped epilogue costs a fraction of such a tile
   // (N = 64 long-K layers too: 7 blocks per tile with per-block commits, -2% on up-C3.a)
   p.nbuf = (fp4 && cv->kp >= 4 && (cv->n_tile == 128 || cv->n_tile == 64)) ? 1 : 2;
+  {
+    // N = 64, any K: one accumulator of 7 blocks with per-block commits (the
+    // epilogue drains block b while later blocks still compute): fewer, taller
+    // tiles amortise the MMA warp's per-tile barrier waits and bias MMAs, which
+    // the tensor core's shallow queue would otherwise expose (measured: stem2
+    // 0.386 -> 0.328 ms, up-C4.b 0.373 -> 0.311 ms), and likewise 3 blocks for
+    // the short-K N = 128 layers (down-C1.a 0.169 -> 0.145, down-C2.a 0.143 ->
+    // 0.120). MBU_SB64=0 / MBU_SB128=0 restore the double-buffered tiles.
+    static const int sb64 = std::getenv("MBU_SB64") ? std::atoi(std::getenv("MBU_SB64")) : 1;
+    static const int sb128 = std::getenv("MBU_SB128") ? std::atoi(std::getenv("MBU_SB128")) : 1;
+    if (fp4 && sb64 && cv->n_tile == 64) p.nbuf = 1;
+    if (fp4 && sb128 && cv->n_tile == 128) p.nbuf = 1;
+  }
   // three accumulator buffers of 2 blocks (N = 64) / 1 block (N = 128): the
   // epilogue of a tile then overlaps two later tiles' MMAs
   // (default: the one-K-stage N = 64 layers, measured -4% on stem2 / up-C3.b / up-C4.b;
