@@ -104,6 +104,7 @@ struct mbu_conv {
   int n_tiles = 0;
   int kc = 0;                    // active 32-lane chunks per pixel
   int chunk_consec = 0;          // bit i: chunk groups of 2^i are consecutive aligned words
+  int tap1_cps = 4;              // one-tap layers: chunks per 128-lane block kept (4, or 2)
   int32_t *d_chunk_word = nullptr;  // [kc] u32 index inside a pixel for each chunk
   int8_t *d_b = nullptr;         // repacked s8 weights, UMMA K-major core-matrix order
   void *d_thr2 = nullptr;        // int2 per GEMM column: bit = (m * acc >= t)

@@ -1287,14 +1287,24 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
   // 3x3: every 32-lane chunk holding a real lane. One tap (1x1, tconv): every
   // chunk of each 128-lane block holding a real lane, so four chunks (16 B of
   // a pixel) form one pipeline stage; pad lanes carry zero weights.
+  // When every block's real lanes lie in its first 64 (a 64-channel input,
+  // e.g. up-CT4's), one-tap stages take just those two chunks (8 B a pixel):
+  // half the expansion and MMA work of whole blocks.
   const int gran = (conv3 ? 32 : 128);
+  int tap1_chunks = 4;
+  if (!conv3) {
+    bool low_half = true;
+    for (int l = 0; l < lpp; ++l) low_half &= !(real[l] && (l & 127) >= 64);
+    if (low_half) tap1_chunks = 2;
+  }
   std::vector<int32_t> chunk_word;
   for (int g0 = 0; g0 < lpp; g0 += gran) {
     bool any = false;
     for (int l = g0; l < g0 + gran; ++l) any |= real[l] != 0;
     if (any)
-      for (int c = g0 / 32; c < (g0 + gran) / 32; ++c) chunk_word.push_back(c);
+      for (int c = g0 / 32; c < g0 / 32 + (conv3 ? 1 : tap1_chunks); ++c) chunk_word.push_back(c);
   }
+  cv->tap1_cps = tap1_chunks;
   const int kc = int(chunk_word.size());
   if (kc == 0 || kc > tc::MAX_CHUNKS) return MBU_OK;
   // bit i: groups of 2^i chunks are consecutive, 2^i-aligned words (one vector copy)
@@ -1729,7 +1739,7 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   // (one TMA box and one commit per block; measured -9% on those layers)
   const bool pps2 = allow_pps2 && fp4 && cv->pair2_ok && cv->n_tile == 128 && p.MB == 1 &&
                     !std::getenv("MBU_FP4_PPS1");
-  const int cps = fp4 ? (pps2 ? 4 : 2) : cv->taps == 1 ? 4 : 1;
+  const int cps = fp4 ? (pps2 ? 4 : 2) : cv->taps == 1 ? cv->tap1_cps : 1;
   const int kcs = fp4 ? 2 * cv->kp : cv->kc;
   if (kcs % cps) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 one-tap conv needs whole 128-lane blocks");
   p.ks = kcs / cps;
@@ -1845,12 +1855,14 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   const int grid = int(std::min<int64_t>(tiles, num_sms()));
   const size_t smem = std::max<size_t>(smem_total, tc::MIN_SMEM);
   if (smem > 227 * 1024) return kNoFit;
+  if (cv->transposed && cps == 2) return launch_tc_impl<1, true, tc::LA_TAP1, 2, false>(p, xmap, xmap2, grid, smem, st);
   if (cv->transposed) return launch_tc_impl<1, true, tc::LA_TAP1, 4, false>(p, xmap, xmap2, grid, smem, st);
   if (fp4 && cps == 4) return launch_tc_impl<9, false, tc::LA_CONV3, 4, true>(p, xmap, xmap2, grid, smem, st);
   if (fp4 && p.nbuf == 1 && p.MB <= 8 && !std::getenv("MBU_NO_BLOCK_COMMIT"))
     return launch_tc_impl<9, false, tc::LA_CONV3, 2, true, true>(p, xmap, xmap2, grid, smem, st);
   if (fp4) return launch_tc_impl<9, false, tc::LA_CONV3, 2, true>(p, xmap, xmap2, grid, smem, st);
   if (cv->taps == 9) return launch_tc_impl<9, false, tc::LA_CONV3, 1, false>(p, xmap, xmap2, grid, smem, st);
+  if (cps == 2) return launch_tc_impl<1, false, tc::LA_TAP1, 2, false>(p, xmap, xmap2, grid, smem, st);
   return launch_tc_impl<1, false, tc::LA_TAP1, 4, false>(p, xmap, xmap2, grid, smem, st);
 }
 
