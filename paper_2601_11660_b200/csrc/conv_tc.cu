@@ -549,7 +549,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       runs_s[nt * 9 + 1 + r++] = make_int4(rn.g, rn.len, rn.o0, (dy << 16) | (rn.tap - dy * p.tconv_s));
       g += rn.len;
     }
-    runs_s[nt * 9] = make_int4(r, 0, 0, 0);
+    // .y: every run starts on a 128-lane block and fills whole 4-group chunks
+    // (or ends its tap, whose pad groups complete the chunk) -> chunked epilogue
+    int chunked = TCONV ? 1 : 0;
+    for (int i = 0; i < r; ++i) {
+      const int4 rn = runs_s[nt * 9 + 1 + i];
+      chunked &= (rn.z % 128 == 0) && (rn.y % 4 == 0 || rn.z / 32 + rn.y == p.c_out_pad / 32);
+    }
+    runs_s[nt * 9] = make_int4(r, chunked, 0, 0);
   }
   if (p.mma_bias) {  // ones slab (16 x 1, 16 x 127 per row) + bias slabs, read by the tensor core
     // (FP4: every entry e2m1 1.0; bias = sum(lo) + 256 * sum(hi), one K = 64 slab per N tile)
@@ -1083,6 +1090,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // whole by one thread instead of two half-sector writes from two warps
       const bool fast_t = TCONV && p.acc == nullptr && p.row_mode && p.tconv_s == 2 && p.c_out_pad == 64 &&
                           p.n_tile == 256 && p.out_groups == 4 && p.bits;
+      // other tconvs: units of (block, run, 4-group chunk) alternate between the
+      // two epilogue halves; each unit is <= 4 TMEM loads + packs and one 16-B
+      // store (both halves busy even when a tile holds a single run)
+      const bool fast_g = TCONV && !fast_t && p.acc == nullptr && p.row_mode && p.bits &&
+                          runs_s[tl.nt * 9].y;
+      if (fast_g) {
+        const int xx = tl.x0 + m;
+        int u = 0;
+        for (int b = 0; b < p.MB; ++b) {
+          const int yy = tl.y0 + b;
+          if constexpr (BLOCK_COMMIT) {
+            mbar_wait(smem_u32(&acc_full[b]), it & 1);
+            tc_fence_after();
+          }
+          const uint32_t colb = lane_base + uint32_t(ab * p.buf_cols + b * p.n_tile);
+          const bool ok = xx < p.w && yy < p.h;
+          const int64_t pix0 = (int64_t(tl.nb) * p.ho + 2 * yy) * p.wo + 2 * xx;
+          for (int ri = 0; ri < nr; ++ri) {
+            const int4 rn = rt[ri];
+            const int64_t opix = pix0 + (rn.w >> 16) * p.wo + (rn.w & 0xFFFF);
+            for (int c = 0; 4 * c < rn.y; ++c, ++u) {
+              if ((u & 1) != half) continue;
+              const int gn = min(4, rn.y - 4 * c);
+              uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                if (q < gn) {
+                  uint32_t v[32];
+                  tmem_ld32(colb + uint32_t((rn.x + 4 * c + q) * 32), v);
+                  w[q] = pack_nonneg<0>(v);
+                }
+              }
+              if (ok)
+                *reinterpret_cast<uint4 *>(p.bits + opix * p.out_stride32 + p.out_off32 + rn.z / 32 + 4 * c) =
+                    make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+        }
+      }
       if (fast_t) {
         const int xx = tl.x0 + m;
         for (int b = 0; b < p.MB; ++b) {
@@ -1135,7 +1181,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       // units (block b, run ri): by block parity when MB >= 2, else by run parity
       const bool split_b = !TCONV || p.MB >= 2;
-      if (!fast && !fast_t)
+      if (!fast && !fast_t && !fast_g)
       for (int b = split_b ? half : 0; b < p.MB; b += split_b ? 2 : 1) {
         // this lane's pixel in block b, once per block
         const int q = block_q0(p, b) + m;

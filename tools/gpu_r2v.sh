@@ -1,2 +1,2 @@
 timeout 900 python -m pytest tests/test_gpu_forward.py tests/test_gpu_layers.py tests/test_gpu_bigshape.py -x -q 2>&1 | tail -1
-bash tools/ab_libs.sh build/ab/base.so build/ab/t2.so
+bash tools/ab_libs.sh build/ab/base.so build/ab/tg.so
