@@ -751,15 +751,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int j = 0; j < PI; ++j) {
         if (j * PROD_THREADS >= p.Q) break;  // (uniform: items past the strip do no work)
           const int q = pt + j * PROD_THREADS;
-          const uint32_t *px = rw + min(q, qbox) * 4;
+          // one 16-B load of the pixel's 128-lane block (a warp reads 512 contiguous
+          // bytes: 4 wavefronts), the stage's chunk words picked in registers --
+          // two 4-B loads at a 16-B stride cost 8 conflicted wavefronts, and the
+          // shared-memory pipe is the MMA's bottleneck here
+          const uint4 r4 = *reinterpret_cast<const uint4 *>(rw + min(q, qbox) * 4);
+          auto word = [&](int c) { return c == 0 ? r4.x : c == 1 ? r4.y : c == 2 ? r4.z : r4.w; };
           const uint32_t keep = ((ec.inb >> j) & 1) ? ~0u : 0u;  // out of bounds -> 0
-          const uint4 e0 = fp4x32(px[ca], keep, s8), e1 = fp4x32(px[cb], keep, s8);
+          const uint4 e0 = fp4x32(word(ca), keep, s8), e1 = fp4x32(word(cb), keep, s8);
           if (q < p.Q) {
             const uint32_t a0 = a_st + q * 16;
             sts128(a0, e0.x, e0.y, e0.z, e0.w);
             sts128(a0 + p.Q * 16, e1.x, e1.y, e1.z, e1.w);
             if constexpr (PPS > 1) {  // the block's second pair: the stage's next A region
-              const uint4 e2 = fp4x32(px[ca2], keep, s8), e3 = fp4x32(px[cb2], keep, s8);
+              const uint4 e2 = fp4x32(word(ca2), keep, s8), e3 = fp4x32(word(cb2), keep, s8);
               sts128(a0 + p.a_chunk_bytes, e2.x, e2.y, e2.z, e2.w);
               sts128(a0 + p.a_chunk_bytes + p.Q * 16, e3.x, e3.y, e3.z, e3.w);
             }
