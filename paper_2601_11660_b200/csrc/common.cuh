@@ -119,6 +119,9 @@ struct mbu_conv {
   int8_t *d_b4 = nullptr;
   int n_slabs4 = 0;
   uint8_t *d_bias_slab4 = nullptr;
+  // CTA-pair copies (conv_tc.cu PAIR): rank-major halves of every B slab, N/2 rows each
+  int8_t *d_b4p = nullptr;
+  uint8_t *d_bias_slab4p = nullptr;
   int32_t *d_slab_of_nt4 = nullptr;
   int8_t *d_bias_slab = nullptr;
   int32_t *d_slab_of_nt = nullptr;

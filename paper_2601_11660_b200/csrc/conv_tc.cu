@@ -158,6 +158,10 @@ struct Params {
   const int32_t *col_bias;  // per GEMM column: TMEM init value
   const int32_t *col_sgn;   // per GEMM column: +-1
   const int32_t *col_w;     // per GEMM column: W (u8 mode) or 0
+  // CTA pair (template PAIR): B rows held per CTA (n_tile / 2; n_tile alone),
+  // spatial tiles per N tile, pair work items (n_tiles * ceil(n_spatial / 2))
+  int b_rows;
+  int n_spatial, n_pairs;
 };
 
 // ----------------------------------------------------------------- PTX glue
@@ -351,6 +355,62 @@ __device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
       : "memory");
 }
+// ---- CTA pair (cta_group::2): the leader's MMAs read A rows 0-127 from its
+// own shared memory and rows 128-255 from its peer's (same offset), B rows
+// [0, N/2) from the leader and [N/2, N) from the peer, and write D rows to
+// each CTA's own TMEM (checked by tools/ubench_pair.cu)
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// the shared::cluster address of `addr` (a shared::cta offset) in CTA `rank`
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
+  // (default .release.cta semantics, the form CUTLASS's ClusterBarrier::arrive uses:
+  // .release.cluster compiles to a MEMBAR.GPU that waits for the epilogue's global stores)
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+__device__ __forceinline__ void mma_fp4_pair(uint32_t d, uint32_t alo, uint32_t ahi, uint32_t blo, uint32_t bhi,
+                                             uint32_t idesc, uint32_t sfa, uint32_t sfb, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 a, b;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %8, 0;\n\t"
+      "mov.b64 a, {%1, %2};\n\t"
+      "mov.b64 b, {%3, %4};\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a, b, %5, [%6], [%7], p;\n\t}" ::"r"(d),
+      "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(sfa), "r"(sfb), "r"(acc)
+      : "memory");
+}
+// commit to the barrier at offset `bar` in both CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          bar),
+      "h"(uint16_t(3))
+      : "memory");
+}
+template <bool PAIR>
+__device__ __forceinline__ void mma_fp4_g(uint32_t d, uint32_t alo, uint32_t ahi, uint32_t blo, uint32_t bhi,
+                                          uint32_t idesc, uint32_t sfa, uint32_t sfb, uint32_t acc) {
+  if constexpr (PAIR) mma_fp4_pair(d, alo, ahi, blo, bhi, idesc, sfa, sfb, acc);
+  else mma_fp4(d, alo, ahi, blo, bhi, idesc, sfa, sfb, acc);
+}
+template <bool PAIR>
+__device__ __forceinline__ void commit_g(uint32_t bar) {
+  if constexpr (PAIR) umma_commit_pair(bar);
+  else umma_commit_elect(bar);
+}
 #define MBU_R32(v)                                                                             \
   "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),      \
       "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),        \
@@ -463,6 +523,17 @@ __device__ __forceinline__ Tile decode_tile(const Params &p, int t) {
   r.x0 = ct * p.TW;
   return r;
 }
+// CTA-pair work item u: N tile u % n_tiles, spatial tiles 2v and 2v + 1
+// (v = u / n_tiles) for ranks 0 and 1 -- one B operand for both halves of the
+// M = 256 MMA. An odd last spatial tile gives rank 1 a copy of it (computed,
+// never stored: valid = false).
+__device__ __forceinline__ int pair_tile(const Params &p, int u, uint32_t rank, bool &valid) {
+  const int v = fdiv(u, p.nt_magic);
+  const int nt = u - v * p.n_tiles;
+  const int sp = 2 * v + int(rank);
+  valid = sp < p.n_spatial;
+  return nt + p.n_tiles * min(sp, p.n_spatial - 1);
+}
 __device__ __forceinline__ int block_q0(const Params &p, int b) {
   return p.row_mode ? (b + p.halo) * p.P + p.halo : p.halo * p.P + p.halo + BLOCK_M * b;
 }
@@ -490,10 +561,18 @@ __device__ __forceinline__ Run run_at(const Params &p, int jt, int g, int groups
 // BLOCK_COMMIT (single-buffered long-K FP4 tiles): the last K stage commits
 // every M block on its own barrier, so the epilogue starts on block 0 while
 // the MMAs of the later blocks still run (-8% on those layers)
-template <int TAPS, bool TCONV, int LA, int CPS, bool FP4, bool BLOCK_COMMIT = false>
+// PAIR (with FP4 + BLOCK_COMMIT, resident weights): a cluster of two CTAs
+// runs M = 256 cta_group::2 MMAs issued by rank 0 -- each CTA expands its own
+// tile's A strip and holds half of B, so every SM's tensor core reads 4 KB of
+// A + N/2 x 32 B of B per MMA instead of 4 KB + N x 32 B (the shared-memory
+// read rate is what bounds the N = 64 MMAs: 49 -> 43 clocks, ubench_pair).
+// Producer and epilogue warps of both CTAs arrive on rank 0's full / acc_empty
+// barriers (one arrive per warp); rank 0's commits multicast to both CTAs.
+template <int TAPS, bool TCONV, int LA, int CPS, bool FP4, bool BLOCK_COMMIT = false, bool PAIR = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap xmap,
                    const __grid_constant__ CUtensorMap xmap2) {
+  static_assert(!PAIR || (FP4 && BLOCK_COMMIT && CPS == 2), "CTA pairs: FP4 single-buffer tiles only");
   constexpr int RAW_STAGES = LA + 1;
   constexpr int PI = prod_items(TAPS);
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -505,7 +584,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t *rfull = bres + 1;       // [8] FP4: raw box landed (TMA)
   uint64_t *rempty = rfull + 8;     // [8] FP4: raw box consumed (producers)
   uint64_t *sf_ready = rempty + 8;  // FP4: the block-scale TMEM columns are written
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sf_ready + 1);
+  uint64_t *pready = sf_ready + 1;  // PAIR (rank 0): the peer's resident weights landed
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(pready + 1);
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  // work items: tiles (u = t) or, PAIR, tile pairs (pair_tile)
+  const int w_first = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int w_step = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
+  const int w_limit = PAIR ? p.n_pairs : p.num_tiles;
+  auto tile_of = [&](int u, bool &valid) -> int {
+    if constexpr (PAIR) return pair_tile(p, u, rank, valid);
+    valid = true;
+    return u;
+  };
+  // arrive on rank 0's copy of a barrier: per warp under PAIR, else per thread
+  auto arrive_lead = [&](uint64_t *bar) {
+    if constexpr (PAIR) {
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
+    } else {
+      mbar_arrive(smem_u32(bar));
+    }
+  };
   int32_t *chunk_s = reinterpret_cast<int32_t *>(smem + 512);  // MAX_CHUNKS words
   uint8_t *a_base = smem + SMEM_HEADER;
   uint8_t *b_base = smem + p.off_b;
@@ -519,10 +618,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(smem_u32(&full[s]), PROD_THREADS + (p.b_resident ? 0 : 1));
+      mbar_init(smem_u32(&full[s]), PAIR ? 2 * NUM_PROD_WARPS : PROD_THREADS + (p.b_resident ? 0 : 1));
       mbar_init(smem_u32(&empty[s]), 1);
     }
     mbar_init(smem_u32(bres), 1);
+    mbar_init(smem_u32(pready), 1);
     for (int i = 0; i < 8; ++i) {
       mbar_init(smem_u32(&rfull[i]), 1);
       mbar_init(smem_u32(&rempty[i]), PROD_THREADS);
@@ -531,7 +631,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(smem_u32(sf_ready), 128);
     }
     for (int i = 0; i < 8; ++i) mbar_init(smem_u32(&acc_full[i]), 1);
-    for (int i = 0; i < 3; ++i) mbar_init(smem_u32(&acc_empty[i]), EPI_THREADS);
+    for (int i = 0; i < 3; ++i) mbar_init(smem_u32(&acc_empty[i]), PAIR ? 2 * NUM_EPI_WARPS : EPI_THREADS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = threadIdx.x; i < p.kc; i += blockDim.x) chunk_s[i] = p.chunk_word[i];
@@ -566,24 +666,51 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     : i < 128 ? make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u)
                               : make_uint4(0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu);
     uint4 *slab = reinterpret_cast<uint4 *>(smem + p.off_slab);
-    const uint4 *src = reinterpret_cast<const uint4 *>(p.bias_slab);
-    for (int i = threadIdx.x; i < p.n_slabs * p.n_tile * 2; i += blockDim.x) slab[i] = src[i];
+    // (PAIR: each CTA holds its B rows of every slab; the rank-major copy)
+    const int slab_u4 = p.n_slabs * p.b_rows * 2;
+    const uint4 *src = reinterpret_cast<const uint4 *>(p.bias_slab) + size_t(rank) * slab_u4;
+    for (int i = threadIdx.x; i < slab_u4; i += blockDim.x) slab[i] = src[i];
     int32_t *smap = reinterpret_cast<int32_t *>(smem + p.off_slabmap);
     for (int i = threadIdx.x; i < p.n_tiles; i += blockDim.x) smap[i] = p.slab_of_nt[i];
     fence_proxy_async();
   }
   if (warp == MMA_WARP) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  // (PAIR: also publishes both CTAs' barrier inits, ones and slabs cluster-wide)
+  if constexpr (PAIR) cluster_sync_all();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if constexpr (FP4) {
+  if constexpr (PAIR) {  // uniform block scales in both CTAs' TMEM before rank 0's first MMA
+    if (warp < 4) {
+      const uint32_t lq = tmem + (uint32_t(warp * 32) << 16);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(lq + p.sf1 + c), "r"(0x7F7F7F7Fu)
+                     : "memory");
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(lq + p.sf256 + c), "r"(0x7F7F877Fu)
+                     : "memory");
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+  } else if constexpr (FP4) {
     // uniform block scales: 4 columns of 2^0 and 4 of 2^8 (any scale layout reads one value)
     if (warp < 4) {
       const uint32_t lq = tmem + (uint32_t(warp * 32) << 16);
@@ -622,9 +749,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int off[PI];
       uint32_t inb = 0;
     };
-    Cache ic, ec;  // issue-side and expand-side tile caches
-    auto tile_offsets = [&](Cache &c, int t) {
-      const Tile tl = decode_tile(p, t);
+    Cache ic, ec;  // issue-side and expand-side tile caches (keyed by work item)
+    auto tile_offsets = [&](Cache &c, int u) {
+      bool tv;
+      const Tile tl = decode_tile(p, tile_of(u, tv));
       c.inb = 0;
 #pragma unroll
       for (int j = 0; j < PI; ++j) {
@@ -636,19 +764,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         c.off[j] = (tl.nb * p.h + iy) * p.w + ix;  // pixel index (the stage picks the tensor)
         if (q < p.Q && rr < strip_rows && iy >= 0 && iy < p.h && ix >= 0 && ix < p.w) c.inb |= 1u << j;
       }
-      c.t = t;
+      c.t = u;
     };
-    // stage g <-> (tile blockIdx.x + (g / ks) * gridDim.x, chunks [cps*(g % ks), +cps))
-    const int tiles_here = p.num_tiles > int(blockIdx.x)
-                               ? (p.num_tiles - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x)
-                               : 0;
+    // stage g <-> (work item w_first + (g / ks) * w_step, chunks [cps*(g % ks), +cps))
+    const int tiles_here = w_limit > w_first ? (w_limit - w_first + w_step - 1) / w_step : 0;
     const int n_stages_total = tiles_here * p.ks;
     constexpr int cps = CPS;
     const int slot_words = p.Q * cps;
     const uint32_t emul = p.u8_act ? 1u : 0xFEu, exr = p.u8_act ? 0u : 0xFFFFFFFFu;
     // incremental cursors (no integer division in the per-stage loop)
-    int i_t = blockIdx.x, i_k = 0, i_slot = 0, i_g = 0;        // issue side
-    int e_t = blockIdx.x, e_k = 0, e_slot = 0, s = 0, ph = 0;  // expand side
+    int i_t = w_first, i_k = 0, i_slot = 0, i_g = 0;        // issue side
+    int e_t = w_first, e_k = 0, e_slot = 0, s = 0, ph = 0;  // expand side
     auto issue = [&]() {
       if (i_g < n_stages_total) {
         if (i_t != ic.t) tile_offsets(ic, i_t);
@@ -702,7 +828,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ++i_g;
       if (++i_k == p.ks) {
         i_k = 0;
-        i_t += gridDim.x;
+        i_t += w_step;
       }
       if (++i_slot == RAW_STAGES) i_slot = 0;
     };
@@ -830,7 +956,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       fence_proxy_async();
-      mbar_arrive(smem_u32(&full[s]));
+      arrive_lead(&full[s]);
       if constexpr (FP4) {
         mbar_arrive(smem_u32(&rempty[rs]));
         if (++rs == p.rraw_stages) {
@@ -847,7 +973,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
       if (++e_k == p.ks) {
         e_k = 0;
-        e_t += gridDim.x;
+        e_t += w_step;
       }
       if (++e_slot == RAW_STAGES) e_slot = 0;
       if (++s == S) {
@@ -860,20 +986,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ============ MMA issue (accumulators pre-loaded with bias) ============
     // The whole warp walks the schedule (all values warp-uniform); one
     // elected lane issues (umma9_i8 / umma1_i8 / umma_commit_elect).
-    {
+    if (PAIR && rank != 0) {  // the peer issues nothing: it reports its resident weights
+      mbar_wait(smem_u32(bres), 0);
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(pready), 0));
+    } else {
       const uint32_t sbo = 128;
       const uint32_t a_lbo = uint32_t(p.Q) * 16;
-      const uint32_t b_lbo = uint32_t(p.n_tile) * 16;
+      const uint32_t b_lbo = uint32_t(p.b_rows) * 16;
       const uint64_t pp = uint64_t(p.P);                        // one strip row, in 16-B units
-      const uint64_t bs = uint64_t(p.n_tile) * 2;               // one tap slab of B, in 16-B units
+      const uint64_t bs = uint64_t(p.b_rows) * 2;               // one tap slab of B, in 16-B units
       const uint64_t a_desc0 = umma_desc(smem_u32(a_base), a_lbo, sbo);
       const uint64_t b_desc0 = umma_desc(smem_u32(b_base), b_lbo, sbo);
       const uint64_t ones_desc = umma_desc(smem_u32(smem + p.off_ones), 128 * 16, sbo);
       const uint64_t slab_desc0 = umma_desc(smem_u32(smem + p.off_slab), b_lbo, sbo);
       const int32_t *smap = reinterpret_cast<const int32_t *>(smem + p.off_slabmap);
       if (p.b_resident) mbar_wait(smem_u32(bres), 0);
+      if constexpr (PAIR) mbar_wait(smem_u32(pready), 0);
       int s = 0, ph = 0, it = 0, ab = 0, aph = 0;  // accumulator buffer ring: index, phase
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+      for (int t = w_first; t < w_limit; t += w_step, ++it) {
+        // (PAIR: t is the work item; both tiles of the pair share its N tile)
         const int nt = t - fdiv(t, p.nt_magic) * p.n_tiles;
         // (read before the wait: a shared load issued behind the tensor core's
         // operand reads takes hundreds of cycles, keep it off the issue path)
@@ -888,12 +1019,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
         const uint32_t d0 = tmem + uint32_t(ab * p.buf_cols);
         if (FP4 && p.mma_bias) {  // bias = lo (K 0-31, A scale 1) + 256 * hi (K 32-63, A scale 2^8)
-          const uint32_t sd = uint32_t(slab_desc0) + uint32_t(slab * p.n_tile * 2);
+          const uint32_t sd = uint32_t(slab_desc0) + uint32_t(slab * p.b_rows * 2);
           for (int b = 0; b < p.MB; ++b)
-            mma_fp4(d0 + uint32_t(b * p.n_tile), uint32_t(ones_desc), uint32_t(ones_desc >> 32), sd,
-                    uint32_t(slab_desc0 >> 32), p.idesc, tmem + p.sf256, tmem + p.sf1, 0u);
+            mma_fp4_g<PAIR>(d0 + uint32_t(b * p.n_tile), uint32_t(ones_desc), uint32_t(ones_desc >> 32), sd,
+                            uint32_t(slab_desc0 >> 32), p.idesc, tmem + p.sf256, tmem + p.sf1, 0u);
         } else if (p.mma_bias) {
-          const uint64_t sd = slab_desc0 + uint64_t(slab) * uint64_t(p.n_tile * 2);
+          const uint64_t sd = slab_desc0 + uint64_t(slab) * uint64_t(p.b_rows * 2);
           for (int b = 0; b < p.MB; ++b) umma1_i8_first(d0 + uint32_t(b * p.n_tile), ones_desc, sd, p.idesc);
         }
 #ifdef MBU_TIMELINE
@@ -928,11 +1059,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const uint32_t bc = b_lo + uint32_t(pr * (p.b_pair_bytes >> 4));
 #pragma unroll
                 for (int tap = 0; tap < 9; ++tap)
-                  mma_fp4(d, ac + uint32_t(tap / 3 - 1) * P32 + uint32_t(tap % 3 - 1), a_hi, bc + uint32_t(tap) * bs32,
-                          b_hi, p.idesc, sf, sf, 1u);
+                  mma_fp4_g<PAIR>(d, ac + uint32_t(tap / 3 - 1) * P32 + uint32_t(tap % 3 - 1), a_hi,
+                                  bc + uint32_t(tap) * bs32, b_hi, p.idesc, sf, sf, 1u);
               }
               if constexpr (BLOCK_COMMIT) {
-                if (k == p.ks - 1) umma_commit_elect(smem_u32(&acc_full[b]));
+                if (k == p.ks - 1) commit_g<PAIR>(smem_u32(&acc_full[b]));
               }
               if (k == 0) MMA_T(2 + b);
             }
@@ -947,7 +1078,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                          a_s + uint64_t(c * (p.a_chunk_bytes >> 4)) + uint64_t(block_q0(p, b)),
                          b_s + uint64_t(c) * bs, p.idesc);
           }
-          umma_commit_elect(smem_u32(&empty[s]));
+          commit_g<PAIR>(smem_u32(&empty[s]));
           if (++s == S) {
             s = 0;
             ph ^= 1;
@@ -972,11 +1103,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncwarp();
   } else if (warp == BLOAD_WARP) {
     // ============ weight stages: one bulk copy per stage ============
-    if (lane == 0 && p.b_resident) {  // every weight stage, once
+    if (lane == 0 && p.b_resident) {  // every weight stage, once (PAIR: this CTA's B rows)
       const uint32_t total = uint32_t(p.n_tiles * p.ks) * p.b_stage_bytes;
+      const int8_t *bsrc = p.b + size_t(rank) * total;
       mbar_arrive_expect_tx(smem_u32(bres), total);
       for (uint32_t off = 0; off < total; off += 32768u)
-        bulk_g2s(smem_u32(b_base + off), p.b + off, min(32768u, total - off), smem_u32(bres));
+        bulk_g2s(smem_u32(b_base + off), bsrc + off, min(32768u, total - off), smem_u32(bres));
     }
     if (lane == 0 && (FP4 || !p.b_resident)) {
       // per stage: the weight slab (streamed) and, FP4, the raw activation box (TMA)
@@ -985,8 +1117,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
         if (p.split32 != 0x7FFFFFFF) asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap2) : "memory");
       }
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        const Tile tl = decode_tile(p, t);
+      for (int u = w_first; u < w_limit; u += w_step) {
+        bool tv;
+        const Tile tl = decode_tile(p, tile_of(u, tv));
         const int8_t *src = p.b + size_t(tl.nt) * p.ks * p.b_stage_bytes;
         for (int k = 0; k < p.ks; ++k, ++g) {
           if constexpr (FP4) {
@@ -1031,7 +1164,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     auto mine = [&](int b, int ri) { return ((p.MB >= 2 ? b : ri) & 1) == half; };
     // bias -> TMEM for every (block, run) unit this warp owns in tile t
     auto init_buffer = [&](int t, int ab) {
-      if (t < p.num_tiles && !p.mma_bias) {
+      if (!PAIR && t < p.num_tiles && !p.mma_bias) {
         const int nt = t - fdiv(t, p.nt_magic) * p.n_tiles;
         const int jt = nt * p.n_tile;
         const int nr = runs_s[nt * 9].x;
@@ -1061,11 +1194,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
       tc_fence_before();
-      mbar_arrive(smem_u32(&acc_empty[ab]));
+      arrive_lead(&acc_empty[ab]);
     };
-    for (int i = 0; i < p.nbuf; ++i) init_buffer(blockIdx.x + i * gridDim.x, i);
+    for (int i = 0; i < p.nbuf; ++i) init_buffer(w_first + i * w_step, i);
     int it = 0, ab = 0, aph = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+    for (int u = w_first; u < w_limit; u += w_step, ++it) {
+      bool tvalid;  // (PAIR: false for rank 1's copy of an odd last tile -- no stores)
+      const int t = tile_of(u, tvalid);
       const Tile tl = decode_tile(p, t);
       // a conv tile is one run of its N tile's groups: no shared-memory table
       // reads on the epilogue path (they queue behind the tensor core's
@@ -1180,7 +1315,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tmem_ld32(colb + 96u, v);
             w3 = pack_nonneg<0>(v);
           }
-          if (xx < p.w && tl.y0 + b < p.h && p.bits)
+          if (tvalid && xx < p.w && tl.y0 + b < p.h && p.bits)
             *reinterpret_cast<uint4 *>(dst0 + b * row_words) = make_uint4(w0, w1, w2, w3);
         }
       }
@@ -1194,7 +1329,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int r = rq - p.halo;
         const int c = q - rq * p.P - p.halo;
         const int yy = tl.y0 + r, xx = tl.x0 + c;
-        const bool valid = r >= 0 && r < p.R && c >= 0 && c < p.TW && yy < p.h && xx < p.w;
+        const bool valid = tvalid && r >= 0 && r < p.R && c >= 0 && c < p.TW && yy < p.h && xx < p.w;
         const int64_t pix0 = TCONV ? (int64_t(tl.nb) * p.ho + yy * p.tconv_s) * p.wo + xx * p.tconv_s
                                    : (int64_t(tl.nb) * p.ho + yy) * p.wo + xx;
         const uint32_t colb = lane_base + uint32_t(ab * p.buf_cols + b * p.n_tile);
@@ -1289,7 +1424,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       EPI_T(10);
       // buffer drained: re-arm it with the bias of the tile that reuses it
-      init_buffer(t + p.nbuf * gridDim.x, ab);
+      init_buffer(u + p.nbuf * w_step, ab);
       if (++ab == p.nbuf) {
         ab = 0;
         aph ^= 1;
@@ -1307,12 +1442,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  // (PAIR: neither CTA leaves while the other may still arrive on its barriers)
+  if constexpr (PAIR) cluster_sync_all();
+  else __syncthreads();
   if (warp == MMA_WARP) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS)
-                 : "memory");
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
   }
 }
 
@@ -1572,6 +1710,29 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
                          "upload fp4 slab map"));
       cv->n_slabs4 = int(slabs.size() / sb);
       for (int i = 0; i < 16 && i < n_tiles; ++i) cv->h_slab_of_nt4[i] = slab_of[i];
+      if (n_tile == 64 || n_tile == 128) {
+        // CTA-pair copies: rank r holds rows [r * n_tile / 2, +n_tile / 2) of every
+        // (n tile, pair, tap) slab and of every bias slab, K halves LBO = n_tile / 2 * 16 apart
+        const int nh = n_tile / 2;
+        const size_t slab_in = size_t(n_tile) * 32, slab_out = size_t(nh) * 32;
+        const size_t n_b = b4.size() / slab_in, n_s = slabs.size() / slab_in;
+        std::vector<uint8_t> b4p(b4.size()), slp(slabs.size());
+        auto split = [&](const std::vector<uint8_t> &in, std::vector<uint8_t> &out, size_t n) {
+          for (int r = 0; r < 2; ++r)
+            for (size_t i = 0; i < n; ++i)
+              for (int half = 0; half < 2; ++half)
+                std::memcpy(&out[(size_t(r) * n + i) * slab_out + size_t(half) * nh * 16],
+                            &in[i * slab_in + size_t(half) * n_tile * 16 + size_t(r) * nh * 16], size_t(nh) * 16);
+        };
+        split(b4, b4p, n_b);
+        split(slabs, slp, n_s);
+        MBU_TRY(check_cuda(cudaMalloc(&cv->d_b4p, b4p.size()), "alloc fp4 pair weights"));
+        MBU_TRY(check_cuda(cudaMemcpy(cv->d_b4p, b4p.data(), b4p.size(), cudaMemcpyHostToDevice),
+                           "upload fp4 pair weights"));
+        MBU_TRY(check_cuda(cudaMalloc(&cv->d_bias_slab4p, slp.size()), "alloc fp4 pair slabs"));
+        MBU_TRY(check_cuda(cudaMemcpy(cv->d_bias_slab4p, slp.data(), slp.size(), cudaMemcpyHostToDevice),
+                           "upload fp4 pair slabs"));
+      }
       cv->kp = kp;
       cv->pair_consec = consec ? 1 : 0;
       // pairs 2j, 2j+1 read the same 128-lane block: one stage can take both
@@ -1649,17 +1810,47 @@ static int num_sms() {
 
 // (a separate trace-free instantiation was tried: ptxas then spills in the
 // epilogue and the N = 64 layers lose ~7%, so trace stays a runtime branch)
-template <int TAPS, bool TCONV, int LA, int CPS, bool FP4, bool BLOCK_COMMIT = false>
+template <int TAPS, bool TCONV, int LA, int CPS, bool FP4, bool BLOCK_COMMIT = false, bool PAIR = false>
 static int launch_tc_impl(const tc::Params &p, const CUtensorMap &xmap, const CUtensorMap &xmap2, int grid,
                           size_t smem, cudaStream_t st) {
+  auto kern = tc::conv_tc_kernel<TAPS, TCONV, LA, CPS, FP4, BLOCK_COMMIT, PAIR>;
   static bool configured = false;
   if (!configured) {
-    MBU_TRY(check_cuda(cudaFuncSetAttribute(tc::conv_tc_kernel<TAPS, TCONV, LA, CPS, FP4, BLOCK_COMMIT>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+    MBU_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
                        "cudaFuncSetAttribute"));
     configured = true;
   }
-  tc::conv_tc_kernel<TAPS, TCONV, LA, CPS, FP4, BLOCK_COMMIT><<<grid, tc::NUM_THREADS, smem, st>>>(p, xmap, xmap2);
+  if constexpr (PAIR) {
+    // persistent clusters of two CTAs (one per SM): as many as can be
+    // co-resident (a GPC with an odd SM count leaves one SM out)
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(tc::NUM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    static const int max_clusters = [&] {
+      cudaLaunchConfig_t q = cfg;
+      q.gridDim = dim3(2 * (num_sms() / 2));
+      q.dynamicSmemBytes = 227 * 1024;  // (one CTA per SM at any size this kernel launches with)
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+      }
+      return n;
+    }();
+    if (max_clusters < 1) return fail(MBU_ERR_CUDA, "conv_tc: no co-resident CTA pair");
+    cfg.gridDim = dim3(2 * std::min(p.n_pairs, max_clusters));
+    MBU_TRY(check_cuda(cudaLaunchKernelEx(&cfg, kern, p, xmap, xmap2), "conv_tc_kernel (CTA pairs)"));
+  } else {
+    kern<<<grid, tc::NUM_THREADS, smem, st>>>(p, xmap, xmap2);
+  }
 #ifdef MBU_TIMELINE
   {
     static int call = 0;
@@ -1694,7 +1885,7 @@ static int launch_tc_impl(const tc::Params &p, const CUtensorMap &xmap, const CU
 constexpr int kNoFit = -1;
 static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
                                uint64_t *bits, int out_stride, int out_offset, cudaStream_t st, bool fp4,
-                               bool allow_pps2);
+                               bool allow_pps2, bool allow_pair);
 int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
                    uint64_t *bits, int out_stride, int out_offset, cudaStream_t st) {
   // 3x3 layers run kind::mxf4 (e2m1) when the uniform block-scale columns fit
@@ -1702,17 +1893,20 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   const bool fp4 = cv->fp4_ok && !g_force_conv_i8 && tc::FP4_COLS / cv->n_tile >= 1;
   if (fp4) {
     for (int allow = 1; allow >= 0; --allow) {  // two pairs per stage if that layout fits, else one
-      const int r = launch_conv_tc_kind(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, true, allow != 0);
-      if (r != kNoFit) return r;
+      for (int pair = 1; pair >= 0; --pair) {  // CTA pairs where eligible and the weights stay resident
+        const int r =
+            launch_conv_tc_kind(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, true, allow != 0, pair != 0);
+        if (r != kNoFit) return r;
+      }
     }
   }
-  const int r = launch_conv_tc_kind(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, false, false);
+  const int r = launch_conv_tc_kind(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, false, false, false);
   return r == kNoFit ? fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv stage does not fit in shared memory") : r;
 }
 
 static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
                                uint64_t *bits, int out_stride, int out_offset, cudaStream_t st, bool fp4,
-                               bool allow_pps2) {
+                               bool allow_pps2, bool allow_pair) {
   tc::Params p{};
   p.x32 = reinterpret_cast<const uint32_t *>(x.base);
   p.n = x.n;
@@ -1791,6 +1985,13 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   const bool pps2 = allow_pps2 && fp4 && cv->pair2_ok && cv->n_tile == 128 && p.MB == 1 &&
                     !std::getenv("MBU_FP4_PPS1");
   const int cps = fp4 ? (pps2 ? 4 : 2) : cv->taps == 1 ? cv->tap1_cps : 1;
+  // CTA pairs (M = 256 MMAs, half of B per CTA) for the single-buffer FP4
+  // tiles with per-block commits; MBU_PAIR=0 keeps one-CTA MMAs
+  static const bool pair_env = !std::getenv("MBU_PAIR") || std::atoi(std::getenv("MBU_PAIR")) != 0;
+  const bool pair = allow_pair && pair_env && fp4 && cps == 2 && p.nbuf == 1 && p.MB <= 8 && cv->d_b4p &&
+                    cv->d_bias_slab4p && (cv->n_tile == 64 || cv->n_tile == 128) &&
+                    !std::getenv("MBU_NO_BLOCK_COMMIT");
+  p.b_rows = pair ? cv->n_tile / 2 : cv->n_tile;
   const int kcs = fp4 ? 2 * cv->kp : cv->kc;
   if (kcs % cps) return fail(MBU_ERR_UNSUPPORTED, "tcgen05 one-tap conv needs whole 128-lane blocks");
   p.ks = kcs / cps;
@@ -1801,8 +2002,8 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
     return fail(MBU_ERR_LAYOUT, "split input view must break at a 128-lane block");
   p.a_chunk_bytes = uint32_t(Q) * 32;
   p.a_stage_bytes = uint32_t((size_t(Q) * 32 * (fp4 ? cps / 2 : cps) + 1023) / 1024 * 1024);
-  p.b_stage_bytes = uint32_t(cv->b_stage_bytes * (fp4 ? cps / 2 : cps));
-  p.b_pair_bytes = uint32_t(cv->b_stage_bytes);
+  p.b_stage_bytes = uint32_t(cv->b_stage_bytes * (fp4 ? cps / 2 : cps) / (pair ? 2 : 1));
+  p.b_pair_bytes = uint32_t(cv->b_stage_bytes / (pair ? 2 : 1));
   const int raw_stages = (cv->taps == 9 ? tc::LA_CONV3 : tc::LA_TAP1) + 1;
   // shared memory: [header][A stages][B stages | resident B][raw ring][runs, biases][ones][slabs][slab map]
   // (FP4: the raw ring holds TMA boxes of one 128-lane block per strip pixel)
@@ -1833,14 +2034,14 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   const size_t raw_bytes = fp4 ? size_t(p.rraw_stages) * p.rraw_bytes : size_t(raw_stages) * Q * cps * 4;
   const size_t runs_bytes = size_t(cv->n_tiles) * 9 * 16 + size_t(cv->n_tiles) * cv->n_tile * 4;
   const int n_slabs = fp4 ? cv->n_slabs4 : cv->n_slabs;
-  const size_t slab_bytes = size_t(n_slabs) * cv->n_tile * 32;
+  const size_t slab_bytes = size_t(n_slabs) * p.b_rows * 32;
   const size_t bias_bytes = n_slabs ? 4096 + slab_bytes + 1024 : 0;
   const size_t budget = 227 * 1024 - tc::SMEM_HEADER - raw_bytes - runs_bytes - bias_bytes - 1024 - 128;
   const size_t b_all = size_t(cv->n_tiles) * p.ks * p.b_stage_bytes;
   p.b_resident = b_all + 3 * size_t(p.a_stage_bytes) <= budget;
   const size_t stage = size_t(p.a_stage_bytes) + (p.b_resident ? 0 : p.b_stage_bytes);
   int stages = int((budget - (p.b_resident ? b_all : 0)) / stage);
-  if (stages < 2) return kNoFit;
+  if (stages < 2 || (pair && !p.b_resident)) return kNoFit;
   p.stages = std::min(stages, tc::MAX_STAGES);
   size_t off = tc::SMEM_HEADER + size_t(p.stages) * p.a_stage_bytes;
   p.off_b = uint32_t(off);
@@ -1853,7 +2054,7 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   off += runs_bytes;
   p.mma_bias = n_slabs > 0;
   p.n_slabs = n_slabs;
-  p.bias_slab = fp4 ? reinterpret_cast<const int8_t *>(cv->d_bias_slab4) : cv->d_bias_slab;
+  p.bias_slab = fp4 ? reinterpret_cast<const int8_t *>(pair ? cv->d_bias_slab4p : cv->d_bias_slab4) : cv->d_bias_slab;
   p.slab_of_nt = fp4 ? cv->d_slab_of_nt4 : cv->d_slab_of_nt;
   for (int i = 0; i < 16 && i < cv->n_tiles; ++i) p.slab_small[i] = fp4 ? cv->h_slab_of_nt4[i] : cv->h_slab_of_nt[i];
   off = (off + 1023) / 1024 * 1024;
@@ -1865,11 +2066,11 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   p.u8_act = cv->pad_mode != MBU_PAD_ZERO;
   p.kc = kcs;
   p.chunk_word = fp4 ? cv->d_chunk_pair : cv->d_chunk_word;
-  p.b = fp4 ? cv->d_b4 : cv->d_b;
+  p.b = fp4 ? (pair ? cv->d_b4p : cv->d_b4) : cv->d_b;
   // instruction descriptor: s32 accum, A u8 (neg_one) / s8 (zero pad), B s8,
   // K-major both, N, M = 128; FP4: block-scaled, A/B e2m1, UE8M0 scales, K = 64
   p.idesc = fp4 ? ((1u << 7) | (1u << 10) | (uint32_t(cv->n_tile >> 3) << 17) | (1u << 23) |
-                   (uint32_t(tc::BLOCK_M >> 4) << 24))
+                   (uint32_t((pair ? 2 : 1) * tc::BLOCK_M >> 4) << 24))
                 : ((2u << 4) | (uint32_t(p.u8_act ? 0 : 1) << 7) | (1u << 10) |
                    (uint32_t(cv->n_tile >> 3) << 17) | (uint32_t(tc::BLOCK_M >> 4) << 24));
   p.sf1 = tc::TMEM_COLS - 8;
@@ -1892,6 +2093,8 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   if (tiles == 0) return MBU_OK;
   if (tiles > 0x7FFFFFFF) return fail(MBU_ERR_SHAPE, "tcgen05 conv grid too large");
   p.num_tiles = int(tiles);
+  p.n_spatial = int(tiles / cv->n_tiles);
+  p.n_pairs = cv->n_tiles * ((p.n_spatial + 1) / 2);
   // magic divisors: umulhi(n, ceil(2^32/d)) == n / d whenever n * d < 2^32
   auto magic = [](int d) { return d == 1 ? 0u : uint32_t((0x100000000ull + d - 1) / d); };
   {
@@ -1909,6 +2112,7 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   if (cv->transposed && cps == 2) return launch_tc_impl<1, true, tc::LA_TAP1, 2, false>(p, xmap, xmap2, grid, smem, st);
   if (cv->transposed) return launch_tc_impl<1, true, tc::LA_TAP1, 4, false>(p, xmap, xmap2, grid, smem, st);
   if (fp4 && cps == 4) return launch_tc_impl<9, false, tc::LA_CONV3, 4, true>(p, xmap, xmap2, grid, smem, st);
+  if (pair) return launch_tc_impl<9, false, tc::LA_CONV3, 2, true, true, true>(p, xmap, xmap2, grid, smem, st);
   if (fp4 && p.nbuf == 1 && p.MB <= 8 && !std::getenv("MBU_NO_BLOCK_COMMIT"))
     return launch_tc_impl<9, false, tc::LA_CONV3, 2, true, true>(p, xmap, xmap2, grid, smem, st);
   if (fp4) return launch_tc_impl<9, false, tc::LA_CONV3, 2, true>(p, xmap, xmap2, grid, smem, st);

@@ -483,6 +483,8 @@ int mbu_conv_destroy(mbu_conv *cv) {
   cudaFree(cv->d_b4);
   cudaFree(cv->d_chunk_pair);
   cudaFree(cv->d_bias_slab4);
+  cudaFree(cv->d_b4p);
+  cudaFree(cv->d_bias_slab4p);
   cudaFree(cv->d_slab_of_nt4);
   cudaFree(cv->d_slab_of_nt);
   delete cv;
