@@ -579,8 +579,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
   uint64_t *empty = full + MAX_STAGES;
   uint64_t *acc_full = empty + MAX_STAGES;
-  uint64_t *acc_empty = acc_full + 8;  // (acc_full[8]: per-block barriers under BLOCK_COMMIT)
-  uint64_t *bres = acc_empty + 4;  // resident weights landed
+  // BLOCK_COMMIT: acc_full[b] / acc_empty[b] per M block of the single buffer
+  // (block b's columns are drained and refilled on their own: the next tile's
+  // MMAs into block 0 start while later blocks are still being drained)
+  uint64_t *acc_empty = acc_full + 8;
+  uint64_t *bres = acc_empty + 8;  // resident weights landed
   uint64_t *rfull = bres + 1;       // [8] FP4: raw box landed (TMA)
   uint64_t *rempty = rfull + 8;     // [8] FP4: raw box consumed (producers)
   uint64_t *sf_ready = rempty + 8;  // FP4: the block-scale TMEM columns are written
@@ -631,7 +634,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(smem_u32(sf_ready), 128);
     }
     for (int i = 0; i < 8; ++i) mbar_init(smem_u32(&acc_full[i]), 1);
-    for (int i = 0; i < 3; ++i) mbar_init(smem_u32(&acc_empty[i]), PAIR ? 2 * NUM_EPI_WARPS : EPI_THREADS);
+    // (BLOCK_COMMIT: a block is drained by the 4 warps of one epilogue half)
+    for (int i = 0; i < 8; ++i)
+      mbar_init(smem_u32(&acc_empty[i]), BLOCK_COMMIT ? (PAIR ? 2 * 4 : 4 * 32) : EPI_THREADS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = threadIdx.x; i < p.kc; i += blockDim.x) chunk_s[i] = p.chunk_word[i];
@@ -1012,18 +1017,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #ifdef MBU_TIMELINE
         unsigned long long tl0 = clock64();
 #endif
-        mbar_wait(smem_u32(&acc_empty[ab]), aph);
+        if constexpr (!BLOCK_COMMIT) mbar_wait(smem_u32(&acc_empty[ab]), aph);
 #ifdef MBU_TIMELINE
         unsigned long long tl1 = clock64();
 #endif
         tc_fence_after();
         const uint32_t d0 = tmem + uint32_t(ab * p.buf_cols);
-        if (FP4 && p.mma_bias) {  // bias = lo (K 0-31, A scale 1) + 256 * hi (K 32-63, A scale 2^8)
-          const uint32_t sd = uint32_t(slab_desc0) + uint32_t(slab * p.b_rows * 2);
+        // bias = lo (K 0-31, A scale 1) + 256 * hi (K 32-63, A scale 2^8)
+        const uint32_t sd = uint32_t(slab_desc0) + uint32_t(slab * p.b_rows * 2);
+        if (FP4 && p.mma_bias && !BLOCK_COMMIT) {  // (BLOCK_COMMIT: per block, in the first K stage)
           for (int b = 0; b < p.MB; ++b)
             mma_fp4_g<PAIR>(d0 + uint32_t(b * p.n_tile), uint32_t(ones_desc), uint32_t(ones_desc >> 32), sd,
                             uint32_t(slab_desc0 >> 32), p.idesc, tmem + p.sf256, tmem + p.sf1, 0u);
-        } else if (p.mma_bias) {
+        } else if (!FP4 && p.mma_bias) {
           const uint64_t sd = slab_desc0 + uint64_t(slab) * uint64_t(p.b_rows * 2);
           for (int b = 0; b < p.MB; ++b) umma1_i8_first(d0 + uint32_t(b * p.n_tile), ones_desc, sd, p.idesc);
         }
@@ -1053,6 +1059,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t bs32 = uint32_t(bs), sf = tmem + p.sf1;
             for (int b = 0; b < p.MB; ++b) {
               const uint32_t d = d0 + uint32_t(b * p.n_tile);
+              if constexpr (BLOCK_COMMIT) {
+                if (k == 0) {  // block b's columns drained (previous tile) -> its bias MMA
+                  mbar_wait(smem_u32(&acc_empty[b]), aph);
+                  tc_fence_after();
+                  mma_fp4_g<PAIR>(d, uint32_t(ones_desc), uint32_t(ones_desc >> 32), sd, uint32_t(slab_desc0 >> 32),
+                                  p.idesc, tmem + p.sf256, tmem + p.sf1, 0u);
+                }
+              }
 #pragma unroll
               for (int pr = 0; pr < CPS / 2; ++pr) {  // chunk pairs of this stage
                 const uint32_t ac = a_lo + uint32_t(block_q0(p, b)) + uint32_t(pr * (p.a_chunk_bytes >> 4));
@@ -1164,6 +1178,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     auto mine = [&](int b, int ri) { return ((p.MB >= 2 ? b : ri) & 1) == half; };
     // bias -> TMEM for every (block, run) unit this warp owns in tile t
     auto init_buffer = [&](int t, int ab) {
+      if constexpr (BLOCK_COMMIT) {  // every block this half drains starts out free
+        tc_fence_before();
+        for (int b = half; b < p.MB; b += 2) arrive_lead(&acc_empty[b]);
+        return;
+      }
       if (!PAIR && t < p.num_tiles && !p.mma_bias) {
         const int nt = t - fdiv(t, p.nt_magic) * p.n_tiles;
         const int jt = nt * p.n_tile;
@@ -1317,6 +1336,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           if (tvalid && xx < p.w && tl.y0 + b < p.h && p.bits)
             *reinterpret_cast<uint4 *>(dst0 + b * row_words) = make_uint4(w0, w1, w2, w3);
+          if constexpr (BLOCK_COMMIT) {  // block b's columns free for the next tile
+            tc_fence_before();
+            arrive_lead(&acc_empty[b]);
+          }
         }
       }
       // units (block b, run ri): by block parity when MB >= 2, else by run parity
@@ -1421,10 +1444,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           if (b == 0) EPI_T(14);
         }
+        if constexpr (BLOCK_COMMIT) {
+          tc_fence_before();
+          arrive_lead(&acc_empty[b]);
+        }
       }
       EPI_T(10);
       // buffer drained: re-arm it with the bias of the tile that reuses it
-      init_buffer(u + p.nbuf * w_step, ab);
+      if constexpr (!BLOCK_COMMIT) init_buffer(u + p.nbuf * w_step, ab);
       if (++ab == p.nbuf) {
         ab = 0;
         aph ^= 1;
