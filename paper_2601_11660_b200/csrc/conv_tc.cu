@@ -568,6 +568,9 @@ __device__ __forceinline__ Run run_at(const Params &p, int jt, int g, int groups
 // read rate is what bounds the N = 64 MMAs: 49 -> 43 clocks, ubench_pair).
 // Producer and epilogue warps of both CTAs arrive on rank 0's full / acc_empty
 // barriers (one arrive per warp); rank 0's commits multicast to both CTAs.
+// Streamed weights: each CTA's weight warp loads its half of every B stage on
+// its own full[s]; rank 1's (otherwise idle) MMA warp forwards each landed
+// stage to rank 0's full[s].
 template <int TAPS, bool TCONV, int LA, int CPS, bool FP4, bool BLOCK_COMMIT = false, bool PAIR = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_tc_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap xmap,
@@ -621,7 +624,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(smem_u32(&full[s]), PAIR ? 2 * NUM_PROD_WARPS : PROD_THREADS + (p.b_resident ? 0 : 1));
+      // (PAIR: rank 0 counts both CTAs' producer warps and B stages; rank 1's
+      // full[s] only tracks its own streamed B stage)
+      mbar_init(smem_u32(&full[s]), PAIR ? (rank == 0 ? 2 * NUM_PROD_WARPS + (p.b_resident ? 0 : 2) : 1)
+                                         : PROD_THREADS + (p.b_resident ? 0 : 1));
       mbar_init(smem_u32(&empty[s]), 1);
     }
     mbar_init(smem_u32(bres), 1);
@@ -991,9 +997,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ============ MMA issue (accumulators pre-loaded with bias) ============
     // The whole warp walks the schedule (all values warp-uniform); one
     // elected lane issues (umma9_i8 / umma1_i8 / umma_commit_elect).
-    if (PAIR && rank != 0) {  // the peer issues nothing: it reports its resident weights
-      mbar_wait(smem_u32(bres), 0);
-      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(pready), 0));
+    if (PAIR && rank != 0) {  // the peer issues nothing: it reports its weights to rank 0
+      if (p.b_resident) {
+        mbar_wait(smem_u32(bres), 0);
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(pready), 0));
+      } else {  // streamed B: forward each landed stage (local full[s]) to rank 0's full[s]
+        const int n_g = (w_limit > w_first ? (w_limit - w_first + w_step - 1) / w_step : 0) * p.ks;
+        int s = 0, ph = 0;
+        for (int g = 0; g < n_g; ++g) {
+          mbar_wait(smem_u32(&full[s]), ph);
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&full[s]), 0));
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
     } else {
       const uint32_t sbo = 128;
       const uint32_t a_lbo = uint32_t(p.Q) * 16;
@@ -1006,7 +1025,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint64_t slab_desc0 = umma_desc(smem_u32(smem + p.off_slab), b_lbo, sbo);
       const int32_t *smap = reinterpret_cast<const int32_t *>(smem + p.off_slabmap);
       if (p.b_resident) mbar_wait(smem_u32(bres), 0);
-      if constexpr (PAIR) mbar_wait(smem_u32(pready), 0);
+      if (PAIR && p.b_resident) mbar_wait(smem_u32(pready), 0);
       int s = 0, ph = 0, it = 0, ab = 0, aph = 0;  // accumulator buffer ring: index, phase
       for (int t = w_first; t < w_limit; t += w_step, ++it) {
         // (PAIR: t is the work item; both tiles of the pair share its N tile)
@@ -1134,7 +1153,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int u = w_first; u < w_limit; u += w_step) {
         bool tv;
         const Tile tl = decode_tile(p, tile_of(u, tv));
-        const int8_t *src = p.b + size_t(tl.nt) * p.ks * p.b_stage_bytes;
+        const int8_t *src = p.b + (size_t(rank) * p.n_tiles + tl.nt) * p.ks * p.b_stage_bytes;
         for (int k = 0; k < p.ks; ++k, ++g) {
           if constexpr (FP4) {
             if (g >= p.rraw_stages) mbar_wait(smem_u32(&rempty[rs]), rph ^ 1);
@@ -1920,7 +1939,7 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
   const bool fp4 = cv->fp4_ok && !g_force_conv_i8 && tc::FP4_COLS / cv->n_tile >= 1;
   if (fp4) {
     for (int allow = 1; allow >= 0; --allow) {  // two pairs per stage if that layout fits, else one
-      for (int pair = 1; pair >= 0; --pair) {  // CTA pairs where eligible and the weights stay resident
+      for (int pair = 1; pair >= 0; --pair) {  // CTA pairs where eligible, else one-CTA tiles
         const int r =
             launch_conv_tc_kind(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, true, allow != 0, pair != 0);
         if (r != kNoFit) return r;
@@ -2068,7 +2087,7 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   p.b_resident = b_all + 3 * size_t(p.a_stage_bytes) <= budget;
   const size_t stage = size_t(p.a_stage_bytes) + (p.b_resident ? 0 : p.b_stage_bytes);
   int stages = int((budget - (p.b_resident ? b_all : 0)) / stage);
-  if (stages < 2 || (pair && !p.b_resident)) return kNoFit;
+  if (stages < 2) return kNoFit;
   p.stages = std::min(stages, tc::MAX_STAGES);
   size_t off = tc::SMEM_HEADER + size_t(p.stages) * p.a_stage_bytes;
   p.off_b = uint32_t(off);
