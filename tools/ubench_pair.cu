@@ -139,7 +139,7 @@ __global__ void pair_check(int N, float *out) {
 }
 
 // rounds of 9 tap-shifted MMAs (A strip of 3 x 130 rows, B one slab per tap), commit per round, 2-deep ring
-template <bool PAIR>
+template <bool PAIR, bool F16 = false>
 __global__ void pair_rate(int N, int reps, unsigned long long *clk) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
@@ -179,8 +179,10 @@ __global__ void pair_rate(int N, int reps, unsigned long long *clk) {
   if (PAIR) cluster_sync(); else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   if (warp == 1 && rank == 0) {
-    const uint32_t idesc = (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (1u << 23) |
-                           (uint32_t((PAIR ? 256 : 128) >> 4) << 24);
+    // F16: kind::f16, f32 accumulator, K = 16 fp16 (the stem's MMA; same 32-B rows)
+    const uint32_t idesc = F16 ? ((1u << 4) | (uint32_t(N >> 3) << 17) | (uint32_t((PAIR ? 256 : 128) >> 4) << 24))
+                               : ((1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (1u << 23) |
+                                  (uint32_t((PAIR ? 256 : 128) >> 4) << 24));
     const uint64_t ad = umma_desc(smem_u32(a) + 131 * 16, Q * 16, 128), bd = umma_desc(smem_u32(b), nb * 16, 128);
     const unsigned long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
@@ -192,7 +194,19 @@ __global__ void pair_rate(int N, int reps, unsigned long long *clk) {
       for (int tap = 0; tap < 9; ++tap) {
         const uint64_t at = ad + uint64_t((tap / 3 - 1) * 130 + (tap % 3 - 1));
         const uint64_t bt = bd + uint64_t(tap * nb * 2);
-        if (PAIR)
+        if (F16 && PAIR)
+          asm volatile(
+              "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+              "l"(at), "l"(bt), "r"(idesc), "r"(tap)
+              : "memory");
+        else if (F16)
+          asm volatile(
+              "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+              "l"(at), "l"(bt), "r"(idesc), "r"(tap)
+              : "memory");
+        else if (PAIR)
           asm volatile(
               "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
               "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n\t}" ::"r"(d),
@@ -283,6 +297,25 @@ int main() {
   }
   unsigned long long *dclk;
   cudaMalloc(&dclk, sms * 8);
+  for (int N : {64, 128})
+    for (int pair = 0; pair <= 1; ++pair) {  // kind::f16, K = 16 (the stem)
+      const int reps = 20000;
+      cudaMemset(dclk, 0, sms * 8);
+      const size_t smem = size_t(3 * 130 + 8) * 32 + 1024 + 9 * N * 32 + 1024;
+      const int grid = sms / 2 * 2;
+      const cudaError_t e = pair ? launch(pair_rate<true, true>, true, grid, smem, N, reps, dclk)
+                                 : launch(pair_rate<false, true>, false, grid, smem, N, reps, dclk);
+      std::vector<unsigned long long> c(sms);
+      cudaMemcpy(c.data(), dclk, sms * 8, cudaMemcpyDeviceToHost);
+      unsigned long long mx = 0;
+      for (auto v : c) mx = v > mx ? v : mx;
+      const double per = double(mx) / (9.0 * reps);
+      const double mac = (pair ? 256.0 * N * 16 / 2 : 128.0 * N * 16) / per;
+      printf("{\"bench\": \"pair_rate_f16\", \"pair\": %d, \"N\": %d, \"err\": \"%s\", \"clk_per_mma\": %.1f, "
+             "\"mac_per_clk_per_sm\": %.0f}\n",
+             pair, N, cudaGetErrorString(e), per, mac);
+      if (e != cudaSuccess) return 1;
+    }
   for (int N : {64, 128, 256})
     for (int pair = 0; pair <= 1; ++pair) {
       const int reps = 20000;
