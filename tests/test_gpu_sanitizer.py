@@ -58,7 +58,13 @@ def test_cta_pair_racecheck_hazards_are_the_pair_tmem_alloc(cuda):
     reported access must sit on the alloc's source line."""
     import re
     src = (ROOT / "paper_2601_11660_b200" / "csrc" / "conv_tc.cu").read_text().splitlines()
-    alloc = {i + 1 for i, l in enumerate(src) if "tcgen05.alloc.cta_group::2" in l}
+    alloc = set()  # every source line of the alloc's asm statement (lineinfo may name any)
+    for i, l in enumerate(src):
+        if "tcgen05.alloc.cta_group::2" in l:
+            j = i
+            while ");" not in src[j]:
+                j += 1
+            alloc |= set(range(i + 1, j + 2))
     assert alloc
     r, out = _run("racecheck", exit_code=False)
     assert r.returncode == 0, out[-4000:]
