@@ -86,8 +86,14 @@ constexpr uint32_t W64_BYTES = 64 * 27 * 8;             // 13824, reference-layo
 constexpr uint32_t CH_BYTES = 64 * 32;                  // per-channel ChanConst
 constexpr uint32_t CONST_BYTES = B_BYTES + W64_BYTES + CH_BYTES;  // one bulk copy
 constexpr int ROW_ELEMS = 3 * RAW_PAIRS;                // 198 doubles per TMA row box
-constexpr int NRAW = 6;               // raw fp64 stages (released by the epilogue)
-constexpr int NA = 2;                 // fp16 A stages
+#ifndef STC_NRAW  // (staging depth as build flags for A/B runs: 3 + 5 / 3 + 4 measured no faster)
+#define STC_NRAW 6
+#endif
+#ifndef STC_NA
+#define STC_NA 2
+#endif
+constexpr int NRAW = STC_NRAW;        // raw fp64 stages (released by the epilogue)
+constexpr int NA = STC_NA;            // fp16 A stages
 constexpr int XRING = 8;              // per-tile max|x| slots
 constexpr int NUM_EPI_WARPS = 8, NUM_PROD_WARPS = 8;
 constexpr int PROD_WARP0 = 8, MMA_WARP = 16, LOAD_WARP = 17;
@@ -276,6 +282,17 @@ __device__ __forceinline__ uint32_t exact_bit(const Params &p, const double *raw
   return yv >= 0.0 ? 1u : 0u;
 }
 
+#ifdef STC_TIMELINE  // per-tile clock64 stamps of CTA 0 (-DSTC_TIMELINE build, printed by the launcher)
+__device__ unsigned long long g_stl[64 * 16];
+#define STL(slot)                                                                          \
+  do {                                                                                     \
+    if (blockIdx.x == 0 && lane == 0 && it < 64) g_stl[it * 16 + (slot)] = clock64();     \
+  } while (0)
+#else
+#define STL(slot) \
+  do {            \
+  } while (0)
+#endif
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     stem_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -334,11 +351,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               smem_u32(smem + OFF_B)),
           "l"(p.b), "r"(CONST_BYTES), "r"(bb)
           : "memory");
-      int rs = 0, rph = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      int rs = 0, rph = 0, it = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         const int nb = t / per_frame, r = t - nb * per_frame;
         const int ty = r / p.col_tiles, tx = r - ty * p.col_tiles;
         mbar_wait(smem_u32(&rempty[rs]), rph ^ 1);
+        STL(0);
         const uint32_t fb = smem_u32(&rfull[rs]);
         mbar_expect_tx(fb, RAW_BYTES);
         const uint32_t dst0 = smem_u32(smem + OFF_RAW + rs * RAW_STRIDE);
@@ -366,8 +384,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int s = 0, ph = 0, it = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
       const int ab = it & 1;
+      STL(1);
       mbar_wait(smem_u32(&acc_empty[ab]), ((it >> 1) & 1) ^ 1);
+      STL(2);
       mbar_wait(smem_u32(&full[s]), ph);
+      STL(3);
       tc_fence_after();
       const uint64_t a_s = a_desc0 + uint64_t((s * A_STRIDE) >> 4);
 #pragma unroll
@@ -375,6 +396,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         umma9_f16(tmem + uint32_t(ab * 256 + b * 64), a_s + uint64_t(b * P), b_desc0, P, p.idesc);
       umma_commit_elect(smem_u32(&empty[s]));
       umma_commit_elect(smem_u32(&acc_full[ab]));
+      STL(4);
       if (++s == NA) {
         s = 0;
         ph ^= 1;
@@ -386,8 +408,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int pt = threadIdx.x - PROD_WARP0 * 32;
     int s = 0, ph = 0, rs = 0, rph = 0, it = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+      if (warp == PROD_WARP0) STL(5);
       mbar_wait(smem_u32(&rfull[rs]), rph);
+      if (warp == PROD_WARP0) STL(6);
       mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+      if (warp == PROD_WARP0) STL(7);
       const double *raw = reinterpret_cast<const double *>(smem + OFF_RAW + rs * RAW_STRIDE);
       const uint32_t a0 = smem_u32(smem + OFF_A + s * A_STRIDE);
       const uint32_t a1 = a0 + QP * 16;
@@ -415,6 +440,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(smem_u32(&full[s]));
+      if (warp == PROD_WARP0) STL(8);
       const uint32_t wmax = __reduce_max_sync(0xffffffffu, __float_as_uint(amax));
       if (lane == 0) {
         xm[(it & (XRING - 1)) * NUM_PROD_WARPS + (warp - PROD_WARP0)] = __uint_as_float(wmax);
@@ -443,13 +469,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int nb = t / per_frame, r = t - nb * per_frame;
       const int ty = r / p.col_tiles, tx = r - ty * p.col_tiles;
       const int slot = it & (XRING - 1);
+      if (warp == 0) STL(9);
       mbar_wait(smem_u32(&xfull[slot]), (it >> 3) & 1);
       float xmax = 0.f;
 #pragma unroll
       for (int i = 0; i < NUM_PROD_WARPS; ++i) xmax = fmaxf(xmax, xm[slot * NUM_PROD_WARPS + i]);
       const float margin = fmaf(xmax, p.m1, p.m0);
       if (it == 0) mbar_wait(smem_u32(bfull), 0);  // channel tables (shared memory)
+      if (warp == 0) STL(10);
       mbar_wait(smem_u32(&acc_full[ab]), (it >> 1) & 1);
+      if (warp == 0) STL(11);
       tc_fence_after();
       mbar_wait(smem_u32(&rfull[rs]), rph);  // orders the TMA-written input for the rechecks
       const double *raw = reinterpret_cast<const double *>(smem + OFF_RAW + rs * RAW_STRIDE);
@@ -499,6 +528,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+      if (warp == 0) STL(12);
+      if (warp == 4) STL(13);
       tc_fence_before();
       mbar_arrive(smem_u32(&acc_empty[ab]));
       mbar_arrive(smem_u32(&rempty[rs]));
@@ -781,6 +812,22 @@ int launch_stem_tc(const mbu_fconv *fc, const double *x, int n, int h, int w, ui
   }
   const int grid = int(std::min<int64_t>(tiles, sms));
   stc::stem_tc_kernel<<<grid, stc::NUM_THREADS, stc::SMEM_BYTES, st>>>(tmap, p);
+#ifdef STC_TIMELINE
+  {
+    unsigned long long h[64 * 16];
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(h, stc::g_stl, sizeof(h));
+    const unsigned long long b0 = h[1];
+    fprintf(stderr, "STEM TIMELINE (CTA 0; clocks from tile 0's MMA start)\n");
+    fprintf(stderr, " it | load:rempty | mma: start accE full done | prod: start rfull empty done | epi0: start xfull accF done | epi4 done\n");
+    for (int i = 0; i < 40; ++i) {
+      const unsigned long long *r = h + i * 16;
+      auto d = [&](int k) { return (long long)(r[k] ? r[k] - b0 : 0); };
+      fprintf(stderr, "%3d | %6lld | %6lld %6lld %6lld %6lld | %6lld %6lld %6lld %6lld | %6lld %6lld %6lld %6lld | %6lld\n", i,
+              d(0), d(1), d(2), d(3), d(4), d(5), d(6), d(7), d(8), d(9), d(10), d(11), d(12), d(13));
+    }
+  }
+#endif
   return check_launch("stem_tc_kernel");
 }
 
