@@ -754,7 +754,9 @@ def run_ours(args):
                        "what": "paper_2601_11660_b200.forward(model, numpy (8,1024,2048,3) float64) -> "
                                "ForwardResult with numpy float64 logits + uint8 mask: the reference's "
                                "graph.forward contract (host arrays in and out, synchronous), host wall "
-                               "clock per call including the pageable 403 MB upload and 151 MB download"}
+                               "clock per call including the 403 MB upload (chunked through a cached "
+                               "page-locked staging buffer) and the 151 MB download (DMA into a cached "
+                               "page-locked buffer, then a host copy into ordinary numpy arrays)"}
                 del imgs
             except Exception as e:  # noqa: BLE001
                 api = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
