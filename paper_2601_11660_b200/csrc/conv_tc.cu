@@ -942,6 +942,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
         }
+      } else if (p.u8_act) {
+        // u8 (the tconvs): out-of-bounds rows were zero-filled by cp.async and
+        // expand to 0, so no mask -- one multiply and one mask per 4 lanes
+#pragma unroll
+        for (int j = 0; j < PI; ++j) {
+          if (j * PROD_THREADS >= p.Q) break;  // (uniform: items past the strip do no work)
+          const int q = pt + j * PROD_THREADS;
+          if (q < p.Q) {
+#pragma unroll
+            for (int c = 0; c < cps; ++c) {
+              const uint32_t a0 = a_st + c * p.a_chunk_bytes + q * 16;
+              const uint32_t b = rw[q * cps + c];
+              sts128(a0, spread4(b & 0xF), spread4((b >> 4) & 0xF), spread4((b >> 8) & 0xF),
+                     spread4((b >> 12) & 0xF));
+              sts128(a0 + p.Q * 16, spread4((b >> 16) & 0xF), spread4((b >> 20) & 0xF), spread4((b >> 24) & 0xF),
+                     spread4(b >> 28));
+            }
+          }
+        }
       } else {
 #pragma unroll
         for (int j = 0; j < PI; ++j) {
