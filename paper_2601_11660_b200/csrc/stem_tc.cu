@@ -95,9 +95,17 @@ constexpr int ROW_ELEMS = 3 * RAW_PAIRS;                // 198 doubles per TMA r
 constexpr int NRAW = STC_NRAW;        // raw fp64 stages (released by the epilogue)
 constexpr int NA = STC_NA;            // fp16 A stages
 constexpr int XRING = 8;              // per-tile max|x| slots
-constexpr int NUM_EPI_WARPS = 8, NUM_PROD_WARPS = 8;
-constexpr int PROD_WARP0 = 8, MMA_WARP = 16, LOAD_WARP = 17;
-constexpr int NUM_THREADS = 18 * 32;
+#ifndef STC_EPI_WARPS  // (A/B build flags: epilogue groups of 4 warps, producer warps)
+#define STC_EPI_WARPS 8
+#endif
+#ifndef STC_PROD_WARPS
+#define STC_PROD_WARPS 8
+#endif
+constexpr int NUM_EPI_WARPS = STC_EPI_WARPS, NUM_PROD_WARPS = STC_PROD_WARPS;
+static_assert(NUM_EPI_WARPS % 4 == 0, "an epilogue group is one warp per TMEM lane quarter");
+constexpr int EPI_GROUPS = NUM_EPI_WARPS / 4;
+constexpr int PROD_WARP0 = NUM_EPI_WARPS, MMA_WARP = PROD_WARP0 + NUM_PROD_WARPS, LOAD_WARP = MMA_WARP + 1;
+constexpr int NUM_THREADS = (LOAD_WARP + 1) * 32;
 constexpr int EPI_THREADS = NUM_EPI_WARPS * 32, PROD_THREADS = NUM_PROD_WARPS * 32;
 constexpr uint32_t OFF_B = 1024;
 constexpr uint32_t OFF_W64 = OFF_B + B_BYTES;
@@ -457,7 +465,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else {
     // ============ epilogue: TMEM -> bits (+ float64 rechecks) ============
-    const int quarter = warp & 3, half = warp >> 2;
+    const int quarter = warp & 3, group = warp >> 2;
     const int m = quarter * 32 + lane;
     const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
     const uint32_t cm0 = uint32_t(p.chmask), cm1 = uint32_t(p.chmask >> 32);
@@ -483,7 +491,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(smem_u32(&rfull[rs]), rph);  // orders the TMA-written input for the rechecks
       const double *raw = reinterpret_cast<const double *>(smem + OFF_RAW + rs * RAW_STRIDE);
 #pragma unroll 1
-      for (int b = half; b < MB; b += 2) {
+      // block b of tile it goes to group (it * MB + b) % EPI_GROUPS
+      for (int b = (group + EPI_GROUPS - (it * MB) % EPI_GROUPS) % EPI_GROUPS; b < MB; b += EPI_GROUPS) {
         uint32_t v[64];
         tmem_ld64(lane_base + uint32_t(ab * 256 + b * 64), v);
         const int y = ty * MB + b, x = tx * TW + m;
