@@ -237,3 +237,21 @@ def test_wide_layers_fp4_cap_and_i8_fallback(cuda):
     assert np.array_equal(fast.logits, traced.logits)
     for name in ("down-C3.a", "down-C4.a", "down-C4.b"):
         assert np.array_equal(traced.trace[name]["acc"], ref[name]["acc"]), name
+
+
+@pytest.mark.parametrize("env", [{"MBU_PAIR": "0"}, {"MBU_SB64": "0", "MBU_SB128": "0"},
+                                 {"MBU_NO_BLOCK_COMMIT": "1"}])
+def test_config1_256_engine_variants(cuda, env):
+    """The engine's tile variants that the default build does not pick (one-CTA
+    tiles instead of CTA pairs; double-buffered tiles; single-buffered tiles
+    without per-block commits) against the same reference digests, each in a
+    fresh process (the switches are read once per process)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    script = Path(__file__).resolve().parent / "run_golden256.py"
+    r = subprocess.run([sys.executable, str(script), "live", "1"], capture_output=True, text=True,
+                       timeout=900, env={**os.environ, **env})
+    assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
+    assert "ok" in r.stdout
