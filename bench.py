@@ -678,6 +678,12 @@ def run_ours(args):
             {"layer": l.name, "kind": l.kind, "ms": round(t, 4),
              "tops": round(o / (t / 1e3) / 1e12, 1) if o and t > 0 else None}
             for l, t, o in zip(model.layers, lt, ops) if l.kind != "concat"]
+        # MBU_FUSED_HEAD=1: the 1x1 head runs inside the epilogue of the conv before it
+        # (no launch of its own); its row then times only the empty event pair
+        if os.environ.get("MBU_FUSED_HEAD") and eng.launches_per_run == sum(
+                l.kind != "concat" for l in model.layers) - 1:
+            breakdown[-1]["fused_into"] = breakdown[-2]["layer"] + " epilogue (its ms include the head)"
+            breakdown[-1]["tops"] = None
         roofline = {
             "bound": "tensor",
             "kernel": ("conv_tc_kernel<9> 3x3 binary convs (tcgen05.mma kind::mxf4, e2m1 "

@@ -69,8 +69,13 @@ int mbu_last_path(void);
  * MBU_OPT_STEM_FFMA: 1 = run the stem through the float32 CUDA-core kernel
  * instead of the tensor-core (fp16-split) kernel; both recheck in float64.
  * MBU_OPT_CONV_I8: 1 = run 3x3 binary convs on kind::i8 instead of kind::mxf4
- * (e2m1 operands); both are exact integer engines for these operands. */
-enum { MBU_OPT_GENERIC_ENDPOINTS = 1, MBU_OPT_STEM_FFMA = 2, MBU_OPT_CONV_I8 = 3 };
+ * (e2m1 operands); both are exact integer engines for these operands.
+ * MBU_OPT_FUSED_HEAD: 1 = run the 1x1 head in the epilogue of the conv that
+ * feeds it instead of as its own kernel (same arithmetic, same results;
+ * measured no faster: the byte-table lookups contend with the tensor core's
+ * shared-memory operand reads, K5). */
+enum { MBU_OPT_GENERIC_ENDPOINTS = 1, MBU_OPT_STEM_FFMA = 2, MBU_OPT_CONV_I8 = 3,
+       MBU_OPT_FUSED_HEAD = 4 };
 int mbu_set_option(int option, int value);
 
 /* ------------------------------------------------------------------ */

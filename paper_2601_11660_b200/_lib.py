@@ -87,6 +87,8 @@ def load(path: str | os.PathLike | None = None):
         fn.argtypes = args
     if os.environ.get("MBU_CONV_I8"):  # A/B switch for benchmarks: 3x3 convs on kind::i8
         lib.mbu_set_option(3, 1)
+    if os.environ.get("MBU_FUSED_HEAD"):  # A/B switch: the head in up-C4.b's epilogue
+        lib.mbu_set_option(4, 1)
     if path is None:
         _lib = lib
     return lib

@@ -24,6 +24,7 @@ extern int g_last_path;
 extern int g_force_generic_fconv;  // mbu_set_option(MBU_OPT_GENERIC_ENDPOINTS)
 extern int g_force_stem_ffma;      // mbu_set_option(MBU_OPT_STEM_FFMA)
 extern int g_force_conv_i8;        // mbu_set_option(MBU_OPT_CONV_I8)
+extern int g_fused_head;           // mbu_set_option(MBU_OPT_FUSED_HEAD)
 
 inline int check_launch(const char *what) {
   cudaError_t e = cudaGetLastError();
@@ -147,11 +148,23 @@ struct mbu_fconv {
 };
 
 namespace mbu {
+// The 1x1 float64 head (graph.py:434-441, 455) folded into the epilogue of the
+// conv that produces its 64-lane input: the conv writes logits + mask instead
+// of the activation words. The caller passes one; the tcgen05 launcher sets
+// `done` when the selected kernel took it (else the head runs on its own).
+struct HeadFuse {
+  const double *tab;  // [8][256] byte-table partial sums (head_prepare)
+  const double *bias; // 1 value, or null
+  double *logits;
+  uint8_t *mask;      // or null
+  bool done;
+};
 // launchers implemented in generic.cu / conv_tc.cu
 int launch_conv_popcount(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
                          uint64_t *bits, int out_stride, int out_offset, cudaStream_t st);
 int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
-                   uint64_t *bits, int out_stride, int out_offset, cudaStream_t st);
+                   uint64_t *bits, int out_stride, int out_offset, cudaStream_t st,
+                   HeadFuse *head = nullptr);
 int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg,
                     const int32_t *seg_off, const int32_t *seg_cnt, int n_seg);
 int launch_maxpool(const ActView &x, uint64_t *out, int out_stride, int out_offset,
@@ -160,7 +173,7 @@ int launch_fconv(const mbu_fconv *fc, const double *x_f64, const ActView &xb, in
                  int w, double *acc, uint64_t *bits, int out_stride, int out_offset,
                  uint8_t *mask, cudaStream_t st);
 int conv_run(mbu_conv *cv, const ActView &x, int32_t *acc, uint64_t *bits, int out_stride,
-             int out_offset, int path, cudaStream_t st);
+             int out_offset, int path, cudaStream_t st, HeadFuse *head = nullptr);
 int stem_prepare(mbu_fconv *fc, const double *w, const double *bias, const double *bn, double eps);
 int launch_stem_fast(const mbu_fconv *fc, const double *x, int n, int h, int w, uint64_t *bits,
                      int out_stride, int out_offset, cudaStream_t st);

@@ -162,6 +162,14 @@ struct Params {
   // spatial tiles per N tile, pair work items (n_tiles * ceil(n_spatial / 2))
   int b_rows;
   int n_spatial, n_pairs;
+  // fused 1x1 float64 head (HeadFuse): the fast N = 64 epilogue turns each
+  // pixel's 64 sign bits into its logit (byte table staged at off_head) and
+  // writes logits + mask instead of the activation words
+  double *head_logits;      // null: no head
+  uint8_t *head_mask;
+  const double *head_tab;   // [8][256]
+  const double *head_bias;  // 1 value, or null
+  uint32_t off_head;
 };
 
 // ----------------------------------------------------------------- PTX glue
@@ -684,6 +692,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int32_t *smap = reinterpret_cast<int32_t *>(smem + p.off_slabmap);
     for (int i = threadIdx.x; i < p.n_tiles; i += blockDim.x) smap[i] = p.slab_of_nt[i];
     fence_proxy_async();
+  }
+  if (p.head_logits) {
+    double2 *ht = reinterpret_cast<double2 *>(smem + p.off_head);
+    const double2 *src = reinterpret_cast<const double2 *>(p.head_tab);
+    for (int i = threadIdx.x; i < 8 * 256 / 2; i += blockDim.x) ht[i] = src[i];
   }
   if (warp == MMA_WARP) {
     if constexpr (PAIR) {
@@ -1372,8 +1385,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tmem_ld32(colb + 96u, v);
             w3 = pack_nonneg<0>(v);
           }
-          if (tvalid && xx < p.w && tl.y0 + b < p.h && p.bits)
+          if (p.head_logits) {
+            // fused head: the same byte-table sum as head_tab64_kernel (bytes
+            // 0-7 of channels 0-63 in order, then the bias), one logit + mask byte
+            if (tvalid && xx < p.w && tl.y0 + b < p.h) {
+              const double *ht = reinterpret_cast<const double *>(smem + p.off_head);
+              double a = 0.0;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const uint32_t word = k < 4 ? w0 : w1;
+                a = __dadd_rn(a, ht[k * 256 + int((word >> (8 * (k & 3))) & 0xFFu)]);
+              }
+              if (p.head_bias) a = __dadd_rn(a, __ldg(p.head_bias));
+              const int64_t pix = (int64_t(tl.nb) * p.ho + tl.y0 + b) * p.wo + xx;
+              __stcs(p.head_logits + pix, a);
+              if (p.head_mask) p.head_mask[pix] = a >= 0.0 ? 1 : 0;
+            }
+          } else if (tvalid && xx < p.w && tl.y0 + b < p.h && p.bits) {
             *reinterpret_cast<uint4 *>(dst0 + b * row_words) = make_uint4(w0, w1, w2, w3);
+          }
           if constexpr (BLOCK_COMMIT) {  // block b's columns free for the next tile
             tc_fence_before();
             arrive_lead(&acc_empty[b]);
@@ -1950,9 +1980,9 @@ static int launch_tc_impl(const tc::Params &p, const CUtensorMap &xmap, const CU
 constexpr int kNoFit = -1;
 static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
                                uint64_t *bits, int out_stride, int out_offset, cudaStream_t st, bool fp4,
-                               bool allow_pps2, bool allow_pair);
+                               bool allow_pps2, bool allow_pair, HeadFuse *head);
 int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
-                   uint64_t *bits, int out_stride, int out_offset, cudaStream_t st) {
+                   uint64_t *bits, int out_stride, int out_offset, cudaStream_t st, HeadFuse *head) {
   // 3x3 layers run kind::mxf4 (e2m1) when the uniform block-scale columns fit
   // next to the accumulators (MB * n_tile <= 248); MBU_OPT_CONV_I8 forces kind::i8
   const bool fp4 = cv->fp4_ok && !g_force_conv_i8 && tc::FP4_COLS / cv->n_tile >= 1;
@@ -1960,18 +1990,20 @@ int launch_conv_tc(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t
     for (int allow = 1; allow >= 0; --allow) {  // two pairs per stage if that layout fits, else one
       for (int pair = 1; pair >= 0; --pair) {  // CTA pairs where eligible, else one-CTA tiles
         const int r =
-            launch_conv_tc_kind(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, true, allow != 0, pair != 0);
+            launch_conv_tc_kind(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, true, allow != 0, pair != 0,
+                                head);
         if (r != kNoFit) return r;
       }
     }
   }
-  const int r = launch_conv_tc_kind(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, false, false, false);
+  const int r =
+      launch_conv_tc_kind(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, false, false, false, nullptr);
   return r == kNoFit ? fail(MBU_ERR_UNSUPPORTED, "tcgen05 conv stage does not fit in shared memory") : r;
 }
 
 static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int wo, int32_t *acc,
                                uint64_t *bits, int out_stride, int out_offset, cudaStream_t st, bool fp4,
-                               bool allow_pps2, bool allow_pair) {
+                               bool allow_pps2, bool allow_pair, HeadFuse *head) {
   tc::Params p{};
   p.x32 = reinterpret_cast<const uint32_t *>(x.base);
   p.n = x.n;
@@ -2032,6 +2064,13 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
     p.MB = ((p.R - 1) * p.P + p.TW + tc::BLOCK_M - 1) / tc::BLOCK_M;
     p.col_tiles = 1;
   }
+  // the head folds into the fast row-mode epilogue of a one-N-tile, 64-column
+  // 3x3 FP4 conv whose output block is channels 0-63 at word 0 (what
+  // head_tab64_kernel reads); anything else leaves it to its own kernel
+  const bool fuse_head = head && head->tab && head->logits && fp4 && !cv->transposed && acc == nullptr &&
+                         p.row_mode && cv->n_tile == 64 && cv->n_gemm == 64 && cv->n_tiles == 1 &&
+                         cv->c_out == 64 && out_stride == 2 && out_offset == 0;
+  const size_t head_bytes = fuse_head ? 8 * 256 * sizeof(double) : 0;
   p.p_magic = uint32_t((0x100000000ull + p.P - 1) / p.P);
   p.buf_cols = fp4 && p.nbuf != 2 ? p.MB * cv->n_tile : tc::ACC_COLS;
   p.row_tiles = (x.h + p.R - 1) / p.R;
@@ -2101,7 +2140,8 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   const int n_slabs = fp4 ? cv->n_slabs4 : cv->n_slabs;
   const size_t slab_bytes = size_t(n_slabs) * p.b_rows * 32;
   const size_t bias_bytes = n_slabs ? 4096 + slab_bytes + 1024 : 0;
-  const size_t budget = 227 * 1024 - tc::SMEM_HEADER - raw_bytes - runs_bytes - bias_bytes - 1024 - 128;
+  const size_t budget =
+      227 * 1024 - tc::SMEM_HEADER - raw_bytes - runs_bytes - bias_bytes - 1024 - 128 - head_bytes;
   const size_t b_all = size_t(cv->n_tiles) * p.ks * p.b_stage_bytes;
   p.b_resident = b_all + 3 * size_t(p.a_stage_bytes) <= budget;
   const size_t stage = size_t(p.a_stage_bytes) + (p.b_resident ? 0 : p.b_stage_bytes);
@@ -2127,6 +2167,15 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   p.off_slab = uint32_t(off + (p.mma_bias ? 4096 : 0));
   p.off_slabmap = uint32_t(p.off_slab + (p.mma_bias ? slab_bytes : 0));
   off = p.off_slabmap + (p.mma_bias ? size_t(cv->n_tiles) * 4 : 0);
+  if (fuse_head) {
+    off = (off + 15) / 16 * 16;
+    p.off_head = uint32_t(off);
+    off += head_bytes;
+    p.head_logits = head->logits;
+    p.head_mask = head->mask;
+    p.head_tab = head->tab;
+    p.head_bias = head->bias;
+  }
   const size_t smem_total = off;
   p.u8_act = cv->pad_mode != MBU_PAD_ZERO;
   p.kc = kcs;
@@ -2174,6 +2223,7 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   const int grid = int(std::min<int64_t>(tiles, num_sms()));
   const size_t smem = std::max<size_t>(smem_total, tc::MIN_SMEM);
   if (smem > 227 * 1024) return kNoFit;
+  if (fuse_head) head->done = true;
   if (cv->transposed && cps == 2) return launch_tc_impl<1, true, tc::LA_TAP1, 2, false>(p, xmap, xmap2, grid, smem, st);
   if (cv->transposed) return launch_tc_impl<1, true, tc::LA_TAP1, 4, false>(p, xmap, xmap2, grid, smem, st);
   if (fp4 && cps == 4) return launch_tc_impl<9, false, tc::LA_CONV3, 4, true>(p, xmap, xmap2, grid, smem, st);

@@ -28,6 +28,7 @@ int g_last_path = 0;
 int g_force_generic_fconv = 0;
 int g_force_stem_ffma = 0;
 int g_force_conv_i8 = 0;
+int g_fused_head = 0;
 
 void set_error(const std::string &msg) { t_last_error = msg; }
 int fail(int status, const std::string &msg) {
@@ -325,7 +326,7 @@ int launch_fconv(const mbu_fconv *fc, const double *x_f64, const ActView &xb, in
 // conv dispatch
 // ---------------------------------------------------------------------------
 int conv_run(mbu_conv *cv, const ActView &x, int32_t *acc, uint64_t *bits, int out_stride,
-             int out_offset, int path, cudaStream_t st) {
+             int out_offset, int path, cudaStream_t st, HeadFuse *head) {
   if (x.wpp != cv->wpp)
     return fail(MBU_ERR_LAYOUT, "input words per pixel " + std::to_string(x.wpp) +
                                     " != weights' " + std::to_string(cv->wpp));
@@ -345,7 +346,7 @@ int conv_run(mbu_conv *cv, const ActView &x, int32_t *acc, uint64_t *bits, int o
     return fail(MBU_ERR_UNSUPPORTED, "tcgen05 path not available for this geometry");
   if (want_tc) {
     g_last_path = MBU_PATH_TCGEN05;
-    return launch_conv_tc(cv, x, ho, wo, acc, bits, out_stride, out_offset, st);
+    return launch_conv_tc(cv, x, ho, wo, acc, bits, out_stride, out_offset, st, head);
   }
   g_last_path = MBU_PATH_POPCOUNT;
   return launch_conv_popcount(cv, x, ho, wo, acc, bits, out_stride, out_offset, st);
@@ -384,6 +385,10 @@ int mbu_set_option(int option, int value) {
   }
   if (option == MBU_OPT_CONV_I8) {
     g_force_conv_i8 = value != 0;
+    return MBU_OK;
+  }
+  if (option == MBU_OPT_FUSED_HEAD) {
+    g_fused_head = value != 0;
     return MBU_OK;
   }
   return fail(MBU_ERR_ENGINE, "unknown option " + std::to_string(option));

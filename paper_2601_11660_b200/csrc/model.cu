@@ -224,9 +224,29 @@ int mbu_forward(mbu_model *m, const double *image, double *logits, uint8_t *mask
                    l.wpp, l.stride, l.offset, nullptr, 0, 0};
   };
   const bool timed = m->timing && int(m->events.size()) == int(m->layers.size()) + 1;
+  // MBU_OPT_FUSED_HEAD: the final 1x1 head folds into the epilogue of the bit
+  // conv right before it when that conv's output feeds nothing else and is not traced
+  auto head_after = [&](int i) -> const mbu_fconv * {
+    const int nl = int(m->layers.size());
+    if (!g_fused_head || g_force_generic_fconv || i + 1 >= nl) return nullptr;
+    const Layer &c = m->layers[i], &h = m->layers[i + 1];
+    if (c.type != MBU_LAYER_BIT_CONV || c.acc_buf >= 0 || h.type != MBU_LAYER_FLOAT_CONV || h.apply_sign ||
+        h.src != i)
+      return nullptr;
+    for (int j = 0; j < nl; ++j)
+      if (j != i + 1 && (m->layers[j].src == i || (m->layers[j].type == MBU_LAYER_CONCAT && m->layers[j].skip == i)))
+        return nullptr;
+    const mbu_fconv *f = h.fconv;
+    if (!f->head_tab || !f->bits_input || f->c_out != 1 || f->c_in != 64 || f->kh != 1 || f->kw != 1 ||
+        f->stride != 1 || f->pad != 0)
+      return nullptr;
+    return f;
+  };
+  int fused_head = -1;
   for (int i = 0; i < int(m->layers.size()); ++i) {
     const Layer &l = m->layers[i];
     if (timed) MBU_TRY(check_cuda(cudaEventRecord(m->events[i], st), "cudaEventRecord"));
+    if (i == fused_head) continue;
     uint64_t *out = l.buf >= 0 ? reinterpret_cast<uint64_t *>(base + m->buf_off[l.buf]) : nullptr;
     void *acc = l.acc_buf >= 0 ? base + m->buf_off[l.acc_buf] : nullptr;
     int in_h = l.src < 0 ? m->H : m->layers[l.src].h;
@@ -244,10 +264,14 @@ int mbu_forward(mbu_model *m, const double *image, double *logits, uint8_t *mask
         break;
       }
       case MBU_LAYER_BIT_CONV:
-      case MBU_LAYER_BIT_TCONV:
+      case MBU_LAYER_BIT_TCONV: {
+        const mbu_fconv *hf = head_after(i);
+        HeadFuse fuse{hf ? hf->d_head_tab : nullptr, hf ? hf->d_bias : nullptr, logits, mask, false};
         MBU_TRY(conv_run(l.conv, view_of(l.src), static_cast<int32_t *>(acc), out, l.stride,
-                         l.offset, path, st));
+                         l.offset, path, st, hf ? &fuse : nullptr));
+        if (fuse.done) fused_head = i + 1;
         break;
+      }
       case MBU_LAYER_MAXPOOL:
         MBU_TRY(launch_maxpool(view_of(l.src), out, l.stride, l.offset, st));
         break;

@@ -17,6 +17,7 @@ steady-state throughput (bench.py).
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 import weakref
 
@@ -257,6 +258,11 @@ def _download(ts, dev) -> list:
     return out
 
 
+def _ws_budget() -> int:
+    """Workspace bytes one forward() call may plan (MBU_FORWARD_WS_BYTES, default 32 GiB)."""
+    return int(os.environ.get("MBU_FORWARD_WS_BYTES", 32 << 30))
+
+
 def forward(model, image, threads: int = 1, trace: bool = False, *, device=None,
             path=_lib.PATH_AUTO):
     """Run the compiled network on an (n, H, W, C) float64 image, on the GPU.
@@ -277,6 +283,17 @@ def forward(model, image, threads: int = 1, trace: bool = False, *, device=None,
     dm = _device_model(model, device)
     n = image.shape[0]
     dev = dm.device
+    if not trace and n > 1:
+        # frames are independent (the reference flattens them into M,
+        # layers.py:276): a batch whose workspace would exceed the budget runs
+        # as consecutive chunks of frames, which also keeps every conv input
+        # under the engine's 2^31-word offsets
+        step = max(1, _ws_budget() // max(1, dm.plan(1, cfg.height, cfg.width, False)))
+        if n > step:
+            parts = [forward(model, image[a:a + step], threads, False, device=dev, path=path)
+                     for a in range(0, n, step)]
+            return _result_cls()(np.concatenate([r.logits for r in parts]),
+                                 np.concatenate([r.mask for r in parts]), None)
     ws_bytes = dm.plan(n, cfg.height, cfg.width, trace)
     with torch.cuda.device(dev):
         ws = torch.empty(max(ws_bytes, 8) // 8 + 1, dtype=torch.int64, device=dev)

@@ -255,3 +255,50 @@ def test_config1_256_engine_variants(cuda, env):
                        timeout=900, env={**os.environ, **env})
     assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
     assert "ok" in r.stdout
+
+
+@pytest.mark.parametrize("n,h,w", [(2, 1024, 2048), (3, 144, 208)])
+def test_fused_head_equals_head_kernel(cuda, n, h, w):
+    """The 1x1 head folded into up-C4.b's epilogue (MBU_OPT_FUSED_HEAD = 1)
+    against the standalone byte-table head kernel (the default): same
+    arithmetic, so logits and masks are identical bit for bit, through both
+    forward() and the CUDA-graph Engine; the fused Engine runs one kernel
+    fewer (144x208: ragged 128-column tiles)."""
+    cfg = mb.UNetConfig(height=h, width=w)
+    rng = np.random.default_rng(5)
+    model = mb.build(cfg, mb.live_bundle(cfg, rng))
+    img = rng.random((n, h, w, 3))
+    plain = mb.forward(model, img)
+    eng_p = mb.Engine(model, batch=n)
+    _lib.call("mbu_set_option", 4, 1)
+    try:
+        fused = mb.forward(model, img)
+        eng_f = mb.Engine(model, batch=n)
+    finally:
+        _lib.call("mbu_set_option", 4, 0)
+    assert np.array_equal(fused.mask, plain.mask)
+    assert np.array_equal(fused.logits.view(np.uint64), plain.logits.view(np.uint64))
+    assert eng_f.launches_per_run == eng_p.launches_per_run - 1
+    for eng in (eng_f, eng_p):
+        eng.image.copy_(torch.from_numpy(img))
+        eng.run()
+    torch.cuda.synchronize()
+    assert torch.equal(eng_f.mask, eng_p.mask)
+    assert torch.equal(eng_f.logits, eng_p.logits)
+    assert np.array_equal(eng_f.logits.cpu().numpy(), fused.logits)
+
+
+def test_forward_chunks_large_batches(cuda, monkeypatch):
+    """forward() splits a batch whose workspace exceeds its budget into
+    consecutive chunks of frames (frames are independent): same logits and
+    masks as one launch sequence over the whole batch."""
+    cfg = mb.UNetConfig(height=144, width=208)
+    rng = np.random.default_rng(9)
+    model = mb.build(cfg, mb.live_bundle(cfg, rng))
+    img = rng.random((5, 144, 208, 3))
+    whole = mb.forward(model, img)
+    ws1 = mb.runtime.DeviceModel(model, cuda).plan(1, 144, 208, False)
+    monkeypatch.setenv("MBU_FORWARD_WS_BYTES", str(2 * ws1))  # two frames per chunk
+    part = mb.forward(model, img)
+    assert np.array_equal(whole.mask, part.mask)
+    assert np.array_equal(whole.logits, part.logits)
