@@ -72,7 +72,7 @@ int mbu_last_path(void);
  * (e2m1 operands); both are exact integer engines for these operands.
  * MBU_OPT_FUSED_HEAD: 1 = run the 1x1 head in the epilogue of the conv that
  * feeds it instead of as its own kernel (same arithmetic, same results;
- * measured no faster: the byte-table lookups contend with the tensor core's
+ * measured slower: the table lookups contend with the tensor core's
  * shared-memory operand reads, K5). */
 enum { MBU_OPT_GENERIC_ENDPOINTS = 1, MBU_OPT_STEM_FFMA = 2, MBU_OPT_CONV_I8 = 3,
        MBU_OPT_FUSED_HEAD = 4 };

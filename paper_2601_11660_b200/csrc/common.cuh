@@ -145,6 +145,7 @@ struct mbu_fconv {
   void *h_stem_tc = nullptr;  // StemTc: device B operand + margins
   int head_tab = 0;           // byte-table head usable (contiguous input lanes from 0)
   double *d_head_tab = nullptr;  // [c_out][ceil(c_in/8)][256] signed partial sums
+  double *d_head_nib = nullptr;  // one-class 64-lane head: [16][16] nibble partial sums
 };
 
 namespace mbu {
@@ -153,7 +154,7 @@ namespace mbu {
 // of the activation words. The caller passes one; the tcgen05 launcher sets
 // `done` when the selected kernel took it (else the head runs on its own).
 struct HeadFuse {
-  const double *tab;  // [8][256] byte-table partial sums (head_prepare)
+  const double *tab;  // [16][16] nibble-table partial sums (head_prepare)
   const double *bias; // 1 value, or null
   double *logits;
   uint8_t *mask;      // or null

@@ -163,11 +163,11 @@ struct Params {
   int b_rows;
   int n_spatial, n_pairs;
   // fused 1x1 float64 head (HeadFuse): the fast N = 64 epilogue turns each
-  // pixel's 64 sign bits into its logit (byte table staged at off_head) and
+  // pixel's 64 sign bits into its logit (nibble tables staged at off_head) and
   // writes logits + mask instead of the activation words
   double *head_logits;      // null: no head
   uint8_t *head_mask;
-  const double *head_tab;   // [8][256]
+  const double *head_tab;   // [16][16] nibble partial sums
   const double *head_bias;  // 1 value, or null
   uint32_t off_head;
 };
@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (p.head_logits) {
     double2 *ht = reinterpret_cast<double2 *>(smem + p.off_head);
     const double2 *src = reinterpret_cast<const double2 *>(p.head_tab);
-    for (int i = threadIdx.x; i < 8 * 256 / 2; i += blockDim.x) ht[i] = src[i];
+    for (int i = threadIdx.x; i < 16 * 16 / 2; i += blockDim.x) ht[i] = src[i];
   }
   if (warp == MMA_WARP) {
     if constexpr (PAIR) {
@@ -1386,16 +1386,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             w3 = pack_nonneg<0>(v);
           }
           if (p.head_logits) {
-            // fused head: the same byte-table sum as head_tab64_kernel (bytes
-            // 0-7 of channels 0-63 in order, then the bias), one logit + mask byte
+            // fused head: the same nibble-table sums as head_nib64_kernel (two
+            // chains over channels 0-31 / 32-63, then the bias), one logit + mask byte
             if (tvalid && xx < p.w && tl.y0 + b < p.h) {
               const double *ht = reinterpret_cast<const double *>(smem + p.off_head);
-              double a = 0.0;
+              double a0 = 0.0, a1 = 0.0;
 #pragma unroll
               for (int k = 0; k < 8; ++k) {
-                const uint32_t word = k < 4 ? w0 : w1;
-                a = __dadd_rn(a, ht[k * 256 + int((word >> (8 * (k & 3))) & 0xFFu)]);
+                a0 = __dadd_rn(a0, ht[k * 16 + int((w0 >> (4 * k)) & 0xFu)]);
+                a1 = __dadd_rn(a1, ht[(8 + k) * 16 + int((w1 >> (4 * k)) & 0xFu)]);
               }
+              double a = __dadd_rn(a0, a1);
               if (p.head_bias) a = __dadd_rn(a, __ldg(p.head_bias));
               const int64_t pix = (int64_t(tl.nb) * p.ho + tl.y0 + b) * p.wo + xx;
               __stcs(p.head_logits + pix, a);
@@ -2070,7 +2071,7 @@ static int launch_conv_tc_kind(const mbu_conv *cv, const ActView &x, int ho, int
   const bool fuse_head = head && head->tab && head->logits && fp4 && !cv->transposed && acc == nullptr &&
                          p.row_mode && cv->n_tile == 64 && cv->n_gemm == 64 && cv->n_tiles == 1 &&
                          cv->c_out == 64 && out_stride == 2 && out_offset == 0;
-  const size_t head_bytes = fuse_head ? 8 * 256 * sizeof(double) : 0;
+  const size_t head_bytes = fuse_head ? 16 * 16 * sizeof(double) : 0;
   p.p_magic = uint32_t((0x100000000ull + p.P - 1) / p.P);
   p.buf_cols = fp4 && p.nbuf != 2 ? p.MB * cv->n_tile : tc::ACC_COLS;
   p.row_tiles = (x.h + p.R - 1) / p.R;

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -322,6 +323,44 @@ __global__ void __launch_bounds__(256) head_tab64_kernel(const uint4 *__restrict
   }
 }
 
+// Same head with sixteen 16-entry nibble tables (2 KB): a half-warp's 16
+// random entries of one table sit in one 128-B row, so every lookup is one
+// conflict-free shared-memory wavefront per half-warp (the 256-entry byte
+// tables take ~3 per half-warp). 16 lookups and adds per pixel instead of 8.
+__global__ void __launch_bounds__(256) head_nib64_kernel(const uint4 *__restrict__ x, const double *__restrict__ tab,
+                                                         const double *__restrict__ bias, int64_t pixels,
+                                                         double *__restrict__ logits, uint8_t *__restrict__ mask) {
+  __shared__ double ts[16 * 16];
+  ts[threadIdx.x] = tab[threadIdx.x];
+  __syncthreads();
+  const double b0 = bias ? __ldg(bias) : 0.0;
+  const int64_t chunk = int64_t(blockDim.x) * 4;
+  for (int64_t base = int64_t(blockIdx.x) * chunk; base < pixels; base += int64_t(gridDim.x) * chunk) {
+    uint4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t q = base + j * blockDim.x + threadIdx.x;
+      v[j] = q < pixels ? __ldcs(x + q) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t q = base + j * blockDim.x + threadIdx.x;
+      double a0 = 0.0, a1 = 0.0;  // two chains: nibbles of channels 0-31 / 32-63
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        a0 = __dadd_rn(a0, ts[k * 16 + int((v[j].x >> (4 * k)) & 0xFu)]);
+        a1 = __dadd_rn(a1, ts[(8 + k) * 16 + int((v[j].y >> (4 * k)) & 0xFu)]);
+      }
+      double acc = __dadd_rn(a0, a1);
+      if (bias) acc = __dadd_rn(acc, b0);
+      if (q < pixels) {
+        __stcs(logits + q, acc);
+        if (mask) mask[q] = acc >= 0.0 ? 1 : 0;
+      }
+    }
+  }
+}
+
 int head_prepare(mbu_fconv *fc, const double *w, const int32_t *lanes) {
   fc->head_tab = 0;
   if (!(fc->bits_input && fc->kh == 1 && fc->kw == 1 && fc->stride == 1 && fc->pad == 0)) return MBU_OK;
@@ -345,6 +384,17 @@ int head_prepare(mbu_fconv *fc, const double *w, const int32_t *lanes) {
   MBU_TRY(check_cuda(cudaMemcpy(fc->d_head_tab, tab.data(), entries * sizeof(double), cudaMemcpyHostToDevice),
                      "upload head table"));
   fc->head_tab = 1;
+  if (fc->c_out == 1 && fc->c_in == 64) {
+    double nib[16 * 16];
+    for (int k = 0; k < 16; ++k)
+      for (int v = 0; v < 16; ++v) {
+        double s = 0.0;
+        for (int i = 0; i < 4; ++i) s += ((v >> i) & 1) ? w[4 * k + i] : -w[4 * k + i];
+        nib[k * 16 + v] = s;
+      }
+    MBU_TRY(check_cuda(cudaMalloc(&fc->d_head_nib, sizeof(nib)), "alloc head nibble table"));
+    MBU_TRY(check_cuda(cudaMemcpy(fc->d_head_nib, nib, sizeof(nib), cudaMemcpyHostToDevice), "upload head nibble table"));
+  }
   return MBU_OK;
 }
 
@@ -355,6 +405,15 @@ int launch_head_fast(const mbu_fconv *fc, const ActView &xb, int n, int h, int w
   if (fc->head_tab && fc->c_out == 1 && (fc->c_in + 7) / 8 == 8 && xb.stride == 2 && xb.offset == 0 &&
       !xb.split && (reinterpret_cast<uintptr_t>(xb.base) & 15) == 0) {
     const int64_t blocks = std::min<int64_t>((pixels + 1023) / 1024, 148 * 8);
+    // 64 lanes: nibble tables (0.131 -> 0.086 ms at the bench shape: the byte
+    // tables' bank conflicts made it shared-memory bound); MBU_HEAD_BYTETAB=1
+    // keeps the byte-table kernel (A/B)
+    static const bool bytetab = std::getenv("MBU_HEAD_BYTETAB") != nullptr;
+    if (!bytetab && fc->d_head_nib) {
+      head_nib64_kernel<<<unsigned(blocks), 256, 0, st>>>(reinterpret_cast<const uint4 *>(xb.base), fc->d_head_nib,
+                                                          fc->d_bias, pixels, logits, mask);
+      return check_launch("head_nib64_kernel");
+    }
     head_tab64_kernel<<<unsigned(blocks), 256, 0, st>>>(reinterpret_cast<const uint4 *>(xb.base), fc->d_head_tab,
                                                         fc->d_bias, pixels, logits, mask);
     return check_launch("head_tab64_kernel");

@@ -580,6 +580,7 @@ int mbu_fconv_destroy(mbu_fconv *fc) {
   stem_free(fc);
   stem_tc_free(fc);
   cudaFree(fc->d_head_tab);
+  cudaFree(fc->d_head_nib);
   delete fc;
   return MBU_OK;
 }

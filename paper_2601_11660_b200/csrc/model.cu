@@ -237,7 +237,7 @@ int mbu_forward(mbu_model *m, const double *image, double *logits, uint8_t *mask
       if (j != i + 1 && (m->layers[j].src == i || (m->layers[j].type == MBU_LAYER_CONCAT && m->layers[j].skip == i)))
         return nullptr;
     const mbu_fconv *f = h.fconv;
-    if (!f->head_tab || !f->bits_input || f->c_out != 1 || f->c_in != 64 || f->kh != 1 || f->kw != 1 ||
+    if (!f->d_head_nib || !f->bits_input || f->c_out != 1 || f->c_in != 64 || f->kh != 1 || f->kw != 1 ||
         f->stride != 1 || f->pad != 0)
       return nullptr;
     return f;
@@ -266,7 +266,7 @@ int mbu_forward(mbu_model *m, const double *image, double *logits, uint8_t *mask
       case MBU_LAYER_BIT_CONV:
       case MBU_LAYER_BIT_TCONV: {
         const mbu_fconv *hf = head_after(i);
-        HeadFuse fuse{hf ? hf->d_head_tab : nullptr, hf ? hf->d_bias : nullptr, logits, mask, false};
+        HeadFuse fuse{hf ? hf->d_head_nib : nullptr, hf ? hf->d_bias : nullptr, logits, mask, false};
         MBU_TRY(conv_run(l.conv, view_of(l.src), static_cast<int32_t *>(acc), out, l.stride,
                          l.offset, path, st, hf ? &fuse : nullptr));
         if (fuse.done) fused_head = i + 1;

@@ -260,7 +260,7 @@ def test_config1_256_engine_variants(cuda, env):
 @pytest.mark.parametrize("n,h,w", [(2, 1024, 2048), (3, 144, 208)])
 def test_fused_head_equals_head_kernel(cuda, n, h, w):
     """The 1x1 head folded into up-C4.b's epilogue (MBU_OPT_FUSED_HEAD = 1)
-    against the standalone byte-table head kernel (the default): same
+    against the standalone nibble-table head kernel (the default): same
     arithmetic, so logits and masks are identical bit for bit, through both
     forward() and the CUDA-graph Engine; the fused Engine runs one kernel
     fewer (144x208: ragged 128-column tiles)."""
