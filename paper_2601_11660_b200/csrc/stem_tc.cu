@@ -141,6 +141,7 @@ struct Params {
   unsigned long long chmask;        // real channels
   int col_tiles, row_tiles, num_tiles;
   uint32_t idesc;
+  int early_release;                // release the accumulator after the tile's last TMEM load
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -490,11 +491,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       mbar_wait(smem_u32(&rfull[rs]), rph);  // orders the TMA-written input for the rechecks
       const double *raw = reinterpret_cast<const double *>(smem + OFF_RAW + rs * RAW_STRIDE);
-#pragma unroll 1
       // block b of tile it goes to group (it * MB + b) % EPI_GROUPS
-      for (int b = (group + EPI_GROUPS - (it * MB) % EPI_GROUPS) % EPI_GROUPS; b < MB; b += EPI_GROUPS) {
+      const int b_first = (group + EPI_GROUPS - (it * MB) % EPI_GROUPS) % EPI_GROUPS;
+      const int b_last = b_first + (MB - 1 - b_first) / EPI_GROUPS * EPI_GROUPS;
+#pragma unroll 1
+      for (int b = b_first; b < MB; b += EPI_GROUPS) {
         uint32_t v[64];
         tmem_ld64(lane_base + uint32_t(ab * 256 + b * 64), v);
+        // the accumulator is in registers once the group's last block is
+        // loaded: free it for the MMA of tile it + 2 before the float64
+        // re-decisions, which then stay off the tensor core's critical path
+        if (p.early_release && b == b_last) {
+          tc_fence_before();
+          mbar_arrive(smem_u32(&acc_empty[ab]));
+        }
         const int y = ty * MB + b, x = tx * TW + m;
         if (y < p.h && x < p.w) {
           float mn = __int_as_float(0x7f800000);
@@ -539,8 +549,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       if (warp == 0) STL(12);
       if (warp == 4) STL(13);
-      tc_fence_before();
-      mbar_arrive(smem_u32(&acc_empty[ab]));
+      if (!p.early_release || b_first >= MB) {
+        tc_fence_before();
+        mbar_arrive(smem_u32(&acc_empty[ab]));
+      }
       mbar_arrive(smem_u32(&rempty[rs]));
       if (++rs == NRAW) {
         rs = 0;
@@ -797,6 +809,8 @@ int launch_stem_tc(const mbu_fconv *fc, const double *x, int n, int h, int w, ui
   p.m1 = k.m1;
   p.m0 = k.m0;
   p.force = k.force;
+  static const bool late = std::getenv("MBU_STEM_LATE_RELEASE") != nullptr;  // (A/B)
+  p.early_release = late ? 0 : 1;
   p.chmask = k.chmask;
   p.col_tiles = (w + stc::TW - 1) / stc::TW;
   p.row_tiles = (h + stc::MB - 1) / stc::MB;
