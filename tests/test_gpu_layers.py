@@ -231,3 +231,19 @@ def test_stem_tc_exact_ties(cuda, shape):
     ref = dense.ref_bn_sign(dense.ref_float_conv(x, w, b, 1, 1), g, be, mean, v, 0.0)
     got = mb.unpack_tensor(mb.BitTensor(*shape, 64, tc.view(np.uint64)))
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("c_in,c_out", [(512, 384), (256, 512), (128, 96)])
+def test_wide_tconv_row_mode_vs_oracle(cuda, rng, c_in, c_out):
+    """2x2/s2 tconvs whose output taps exceed one 256-column N tile (up-CT1:
+    384 channels, tiles that straddle two taps) at row-mode widths (>= 128
+    columns, including a ragged column tile) against the dense oracle."""
+    for h, w in [(2, 128), (3, 136)]:
+        x = rng.choice((-1, 1), size=(2, h, w, c_in)).astype(np.int8)
+        wt = rng.choice((-1, 0, 1), size=(c_out, 2, 2, c_in)).astype(np.int8)
+        xt = mb.pack_tensor(x)
+        planes = mb.pack_conv_weights(wt, xt.segments, masked=True)
+        spec = mb.ConvSpec(2, 2, 2, 0, c_in, c_out)
+        got = mb.transposed_conv_forward(xt, planes, spec)
+        ref = dense.ref_tconv(x, wt, 2)
+        assert np.array_equal(got, ref), (c_in, c_out, h, w)
