@@ -1235,6 +1235,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         return;
       }
       if (!PAIR && t < p.num_tiles && !p.mma_bias) {
+        if constexpr (TCONV) {
+          // a tconv's runs are owned by run parity and may sit on different
+          // columns in the tile that reuses the buffer: wait until both halves
+          // have drained it before either writes the next tile's bias
+          tc_fence_before();
+          asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
+          tc_fence_after();
+        }
         const int nt = t - fdiv(t, p.nt_magic) * p.n_tiles;
         const int jt = nt * p.n_tile;
         const int nr = runs_s[nt * 9].x;
@@ -1613,6 +1621,10 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
   int n_tile;
   if (!cv->transposed) n_tile = std::min(c_out_pad, 128);
   else if (c_out_pad <= 256) n_tile = c_out_pad * std::min(s2, 256 / c_out_pad);
+  // wider taps in 256-column tiles of 128-aligned runs (up-CT1, 384 channels:
+  // 6 N tiles instead of 12, so each A strip is expanded half as often);
+  // MBU_TCONV_N128=1 keeps 128-column slices (A/B)
+  else if (c_out_pad % 128 == 0 && !std::getenv("MBU_TCONV_N128")) n_tile = 256;
   else if (c_out_pad % 128 == 0) n_tile = 128;
   else if (c_out_pad % 64 == 0) n_tile = 64;
   else n_tile = 32;
