@@ -1888,7 +1888,9 @@ int prepare_conv_tc(mbu_conv *cv, const uint64_t *pos, const uint64_t *neg, cons
       }
       slab_of[nt] = found;
     }
-    if (slabs.size() <= 16384) {
+    // (32 KB: up-CT1's 3 and up-CT2's distinct per-tap slabs take the bias MMA
+    // too, so their epilogues never write TMEM; 16 KB measured ~5 % slower on up-CT2)
+    if (slabs.size() <= 32768) {
       MBU_TRY(check_cuda(cudaMalloc(&cv->d_bias_slab, slabs.size()), "alloc bias slabs"));
       MBU_TRY(check_cuda(cudaMemcpy(cv->d_bias_slab, slabs.data(), slabs.size(), cudaMemcpyHostToDevice),
                          "upload bias slabs"));
